@@ -1,0 +1,212 @@
+/* spmk_capi.h — C ABI of the B200-native adaptive SpMV/SpMM engine.
+ *
+ * Drop-in boundary for the reference's hot path (arxiv 2106.16064 artifact
+ * `spmk`, /root/reference/proj/include/spmk).  Every entry point below names
+ * the reference interface it replaces.  Plain C types only (no torch, no STL):
+ * host pointers are `const int64_t*`/`const float*`, device pointers are
+ * `d_`-prefixed, streams are passed as `void*` (a cudaStream_t).
+ *
+ * Value type: fp32 only (the reference's `T=float` instantiation).  T=double is
+ * SPMK_EUNSUPPORTED — there is no CPU fallback.  Indices are narrowed to int32
+ * on the device (every BASELINE config has nnz < 2^31; larger is
+ * SPMK_EUNSUPPORTED).
+ *
+ * Errors: every call returns spmk_status; the message of the last failure on
+ * the calling thread is spmk_last_error().  The C++ drop-in headers
+ * (include/spmk/*.hpp) rethrow it as spmk::Error (error.hpp:10-13).
+ *
+ * Threading: calls are thread-safe on distinct handles; a handle is bound to
+ * the CUDA device it was created on.
+ */
+#ifndef SPMK_CAPI_H
+#define SPMK_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMK_CAPI_VERSION 1
+
+typedef enum {
+  SPMK_OK = 0,
+  SPMK_EINVAL = 1,       /* bad argument / config (kernels.hpp:91-100)      */
+  SPMK_EDIM = 2,         /* dimension mismatch (kernels.hpp:103-109)         */
+  SPMK_ECUDA = 3,        /* CUDA runtime error                               */
+  SPMK_ENOMEM = 4,       /* device allocation failed                         */
+  SPMK_ENCCL = 5,        /* reserved: collective failure                     */
+  SPMK_EUNSUPPORTED = 6  /* valid for the reference, not on this device path */
+} spmk_status;
+
+/* kernel_index numbering, kernels.hpp:47-50: 2*seq + ws.
+ * Names kernels.hpp:40-45: "par-rs", "par-ws", "seq-rs", "seq-ws". */
+typedef enum {
+  SPMK_PAR_ROWSPLIT = 0, /* kParRowSplit kernels.hpp:29  (north_star b) */
+  SPMK_PAR_BALANCED = 1, /* kParBalanced kernels.hpp:31  (north_star d, VSR) */
+  SPMK_SEQ_ROWSPLIT = 2, /* kSeqRowSplit kernels.hpp:33  (north_star a, CSC) */
+  SPMK_SEQ_BALANCED = 3  /* kSeqBalanced kernels.hpp:35  (north_star c) */
+} spmk_kernel_id;
+
+/* KernelConfig, kernels.hpp:81-87 — same fields, same order, same defaults.
+ * worker_count is accepted and ignored on the device (the CUDA grid replaces
+ * the ThreadPool); stats are computed analytically (spmk_kernel_stats). */
+typedef struct {
+  uint64_t lane_width;   /* W: power of two in [2, 64]; default 32          */
+  uint64_t vdl_group;    /* C in {0 (auto), 1, 2, 4}; default 0             */
+  uint64_t seq_chunk;    /* nonzeros per seq-ws chunk (>= 1); default 256   */
+  uint64_t worker_count; /* ignored on device                               */
+} spmk_kernel_config;
+
+/* SelectorThresholds, selector.hpp:16-22 */
+typedef struct {
+  uint64_t n_parallel_max; /* default 4    */
+  double t_parallel_avg;   /* default 32.0 */
+  double t_cv;             /* default 1.0  */
+} spmk_thresholds;
+
+/* MatrixFeatures, csr.hpp:86-92 */
+typedef struct {
+  double avg_row;
+  double stdv_row;
+  double cv;
+  int64_t num_rows;
+  int64_t nnz;
+} spmk_features;
+
+typedef struct spmk_csr_s* spmk_csr_t;
+
+/* ------------------------------------------------------------ library */
+const char* spmk_last_error(void);
+int spmk_version(void);
+void spmk_default_config(spmk_kernel_config* cfg);   /* KernelConfig{}       */
+void spmk_default_thresholds(spmk_thresholds* t);    /* SelectorThresholds{} */
+/* kernels.hpp:91-100 check_config */
+spmk_status spmk_check_config(const spmk_kernel_config* cfg);
+/* kernels.hpp:40-45 kernel_name / :52-57 parse_kernel */
+const char* spmk_kernel_name(spmk_kernel_id id);
+spmk_status spmk_parse_kernel(const char* name, spmk_kernel_id* out);
+
+/* ------------------------------------------------------------ operand A */
+/* Replaces CsrMatrix<float> (csr.hpp:24-57) + validate (csr.hpp:95-119):
+ * validates the HOST arrays (int64, reference layout), uploads them to
+ * `device`, narrows indices to int32 and builds the handle's resident row
+ * metadata (non-empty row compaction, empty-row list). */
+spmk_status spmk_csr_create(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx,
+                            const float* values, int device, spmk_csr_t* out);
+/* Same, from int32 DEVICE arrays already in HBM (e.g. the device generator).
+ * copy=0 borrows the arrays (caller keeps them alive), copy=1 duplicates.
+ * Validation is done on the device (canonical rows, bounds). */
+spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols,
+                                   int64_t nnz, const int32_t* d_row_ptr,
+                                   const int32_t* d_col_idx,
+                                   const float* d_values, int copy,
+                                   spmk_csr_t* out);
+/* Row slice [row_begin, row_end) of `a` as a standalone rebased CSR on
+ * `device` (multi-GPU equal-nnz slices). */
+spmk_status spmk_csr_slice(spmk_csr_t a, int64_t row_begin, int64_t row_end,
+                           int device, spmk_csr_t* out);
+spmk_status spmk_csr_destroy(spmk_csr_t a);
+spmk_status spmk_csr_info(spmk_csr_t a, int64_t* num_rows, int64_t* num_cols,
+                          int64_t* nnz, int64_t* max_row_nnz,
+                          int64_t* empty_rows);
+/* Device pointers of the resident int32 CSR (rowPtr, colIdx, values). */
+spmk_status spmk_csr_device_arrays(spmk_csr_t a, const int32_t** d_row_ptr,
+                                   const int32_t** d_col_idx,
+                                   const float** d_values);
+/* Download back to the reference layout (int64 indices). */
+spmk_status spmk_csr_download(spmk_csr_t a, int64_t* row_ptr, int64_t* col_idx,
+                              float* values);
+
+/* ------------------------------------------------------------ selection */
+/* extract_features (csr.hpp:166-181): device reduction of exact integer
+ * row-length moments, host finalize.  avg_row is bit-identical to the
+ * reference; stdv_row/cv agree to ~1e-12 relative (SURVEY §8a tie-guard). */
+spmk_status spmk_features_compute(spmk_csr_t a, spmk_features* out);
+/* The same on host row_ptr, in the reference's exact sequential order. */
+spmk_status spmk_features_host(int64_t num_rows, const int64_t* row_ptr,
+                               spmk_features* out);
+/* select_kernel (selector.hpp:28-34).  t may be NULL (defaults). */
+spmk_kernel_id spmk_select(const spmk_features* f, uint64_t n,
+                           const spmk_thresholds* t);
+/* features + select on the handle, with the tie-guard: when cv (or avg_row)
+ * lies within 1e-9 relative of its threshold, features are recomputed in the
+ * reference's sequential order so the choice is bit-exact. */
+spmk_status spmk_select_for(spmk_csr_t a, uint64_t n, const spmk_thresholds* t,
+                            spmk_kernel_id* out);
+
+/* ------------------------------------------------------------ partition */
+/* plan_balanced (kernels.hpp:133-149) without the COO expansion: computed on
+ * the device as upper_bound(rowPtr, q*chunk)-1.  chunk_first_row (host, may be
+ * NULL) receives elem_row[q*chunk] for every chunk q; num_chunks =
+ * ceil(nnz/chunk). */
+spmk_status spmk_plan(spmk_csr_t a, int64_t chunk, int64_t* chunk_first_row,
+                      int64_t* num_chunks);
+/* Full elem_row expansion (host out, nnz entries) for parity tests. */
+spmk_status spmk_plan_elem_row(spmk_csr_t a, int64_t* elem_row);
+/* detail::partition (kernels.hpp:124-129) */
+void spmk_partition(int64_t items, int64_t parts, int64_t w, int64_t* lo,
+                    int64_t* hi);
+/* Equal-nnz row slices for `parts` devices: bounds[parts+1] (host), bounds[g] =
+ * lower_bound(rowPtr, partition(nnz, parts, g).lo); computed on the device. */
+spmk_status spmk_row_slices(spmk_csr_t a, int64_t parts, int64_t* bounds);
+
+/* ------------------------------------------------------------ SpMM */
+/* spmm(KernelId, A, X, cfg) (kernels.hpp:457-464) on resident operands:
+ * Y (num_rows x n, row-major, fp32, DEVICE) = A * X (num_cols x n, DEVICE).
+ * Y is fully overwritten (empty rows get 0).  cfg may be NULL (defaults).
+ * Asynchronous on `stream` (NULL = legacy default stream).  Results are
+ * bit-identical to the reference's fp32 kernel of the same KernelId at the
+ * same lane_width / seq_chunk (same partials, same summation order). */
+spmk_status spmk_spmm(spmk_csr_t a, spmk_kernel_id id,
+                      const spmk_kernel_config* cfg, const float* d_x,
+                      int64_t n, float* d_y, void* stream);
+/* Rule-selected variant (select_for + spmm).  chosen may be NULL. */
+spmk_status spmk_spmm_auto(spmk_csr_t a, const spmk_thresholds* t,
+                           const spmk_kernel_config* cfg, const float* d_x,
+                           int64_t n, float* d_y, void* stream,
+                           spmk_kernel_id* chosen);
+/* Host X in, host Y out (h2d, kernel, d2h on `stream`, then synchronize):
+ * the value-returning reference call shape.  Staging buffers are cached in
+ * the handle. */
+spmk_status spmk_spmm_host(spmk_csr_t a, spmk_kernel_id id,
+                           const spmk_kernel_config* cfg, const float* x,
+                           int64_t n, float* y, void* stream);
+/* One-shot drop-in for `spmm(id, CsrMatrix, DenseMatrix, cfg)` with every
+ * operand on the host (create handle on `device`, run, download, destroy). */
+spmk_status spmk_spmm_csr_host(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                               const int64_t* row_ptr, const int64_t* col_idx,
+                               const float* values, spmk_kernel_id id,
+                               const spmk_kernel_config* cfg, const float* x,
+                               int64_t n, float* y, int device);
+
+/* KernelStats (kernels.hpp:67-79), computed analytically with the reference's
+ * lockstep formulas (:187, :200-201, :283-285). */
+spmk_status spmk_kernel_stats(spmk_csr_t a, spmk_kernel_id id,
+                              const spmk_kernel_config* cfg, int64_t n,
+                              uint64_t* lane_multiplies, uint64_t* scan_ops);
+/* kernel_tolerance<float> (kernels.hpp:468-472) */
+double spmk_kernel_tolerance(int64_t max_row_nnz);
+
+/* Pin X in L2 for subsequent spmk_spmm calls on `stream`: an access-policy
+ * window over d_x (persisting hits, streaming misses), clamped to the
+ * device's max window / persisting-L2 size.  bytes=0 clears the window. */
+spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes);
+
+/* ------------------------------------------------------------ generators */
+/* generate_rmat<float> (rmat.hpp:61-88 + csr.hpp:123-164) on the device,
+ * bit-identical to the reference (counter form of SplitMix64): returns a
+ * handle owning int32 rowPtr/colIdx and values = 1. */
+spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a,
+                               double b, double c, double d, uint64_t seed,
+                               int device, spmk_csr_t* out);
+/* make_dense<float> (corpus.hpp:116-122) on the device: d_out[rows*cols]. */
+spmk_status spmk_make_dense(int64_t rows, int64_t cols, uint64_t seed,
+                            float* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPMK_CAPI_H */

@@ -1,0 +1,213 @@
+// aux_kernels.cuh — partition, features, row metadata, fix-up, zero-fill and
+// validation kernels (integer work; bit-exact by construction).
+#pragma once
+#include "common.cuh"
+
+namespace spmk_dev {
+
+__device__ __forceinline__ long long lower_bound_i32(const int* __restrict__ a,
+                                                     long long n, long long v) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if ((long long)a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ long long upper_bound_i32(const int* __restrict__ a,
+                                                     long long n, long long v) {
+  long long lo = 0, hi = n;
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if ((long long)a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// int64 (reference Index) -> int32 device narrowing, with overflow flag.
+__global__ void narrow_kernel(const long long* __restrict__ in, int* __restrict__ out,
+                              long long n, int* __restrict__ bad) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long v = in[i];
+    if (v < INT32_MIN || v > INT32_MAX) *bad = 1;
+    out[i] = (int)v;
+  }
+}
+__global__ void widen_kernel(const int* __restrict__ in, long long* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+// validate (csr.hpp:95-119) on the device.  err bits: 1 row_ptr, 2 column
+// range, 4 column order.
+__global__ void validate_kernel(const int* __restrict__ rp, const int* __restrict__ col,
+                                int m, int k, long long nnz, int* __restrict__ err) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = rp[i], f = rp[i + 1];
+    if (s > f || s < 0 || f > nnz) { atomicOr(err, 1); continue; }
+    for (int e = s; e < f; ++e) {
+      const int c = col[e];
+      if (c < 0 || c >= k) atomicOr(err, 2);
+      if (e > s && c <= col[e - 1]) atomicOr(err, 4);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (rp[0] != 0 || (long long)rp[m] != nnz) atomicOr(err, 1);
+  }
+}
+
+// row-length moments for extract_features (csr.hpp:166-181): exact integer
+// sums sum(len), sum(len^2), max(len).  Order-independent => deterministic.
+__global__ void row_moments_kernel(const int* __restrict__ rp, int m,
+                                   unsigned long long* __restrict__ out /*3*/) {
+  unsigned long long s1 = 0, s2 = 0, mx = 0, ne = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long l = (unsigned long long)(rp[i + 1] - rp[i]);
+    s1 += l;
+    s2 += l * l;
+    mx = l > mx ? l : mx;
+    ne += l == 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+    ne += __shfl_xor_sync(0xffffffffu, ne, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out + 0, s1);
+    atomicAdd(out + 1, s2);
+    atomicMax(out + 2, mx);
+    atomicAdd(out + 3, ne);
+  }
+}
+
+// Non-empty row compaction: flags -> (exclusive scan on host-driven CUB) ->
+// scatter.  crp[pos] = rp[i] for non-empty rows, erow = empty rows.
+__global__ void nonempty_flag_kernel(const int* __restrict__ rp, int m, int* __restrict__ flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    flag[i] = rp[i + 1] > rp[i] ? 1 : 0;
+}
+__global__ void compact_scatter_kernel(const int* __restrict__ rp, int m,
+                                       const int* __restrict__ pos /*exclusive scan*/,
+                                       int* __restrict__ crp, int* __restrict__ rid,
+                                       int* __restrict__ erow) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int p = pos[i];
+    if (rp[i + 1] > rp[i]) {
+      crp[p] = rp[i];
+      rid[p] = (int)i;
+    } else {
+      erow[i - p] = (int)i;
+    }
+  }
+}
+
+// Tile plan: rlo[t] = lower_bound(crp, t*TS) for t < ntiles, rlo[ntiles] = mne.
+__global__ void tile_plan_kernel(const int* __restrict__ crp, int mne, long long ntiles,
+                                 long long TS, int* __restrict__ rlo) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t <= ntiles;
+       t += (long long)gridDim.x * blockDim.x) {
+    rlo[t] = (t == ntiles) ? mne : (int)lower_bound_i32(crp, (long long)mne + 1, t * TS);
+  }
+}
+// Long rows for a tile size: rows spanning >= 2 tile boundaries past their own.
+__global__ void long_rows_kernel(const int* __restrict__ crp, int mne, long long TS,
+                                 int* __restrict__ list, int* __restrict__ count) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < mne;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long s = crp[c], f = crp[c + 1];
+    if ((f - 1) / TS - s / TS >= 2) list[atomicAdd(count, 1)] = (int)c;
+  }
+}
+// plan_balanced (kernels.hpp:133-149) chunk starts: elem_row[q*chunk] =
+// upper_bound(rowPtr, q*chunk) - 1.
+__global__ void chunk_first_row_kernel(const int* __restrict__ rp, int m, long long nchunks,
+                                       long long chunk, long long* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nchunks;
+       q += (long long)gridDim.x * blockDim.x)
+    out[q] = upper_bound_i32(rp, (long long)m + 1, q * chunk) - 1;
+}
+// Full elem_row expansion (parity tests only).
+__global__ void elem_row_kernel(const int* __restrict__ rp, int m, long long nnz,
+                                long long* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = upper_bound_i32(rp, (long long)m + 1, e) - 1;
+}
+// Multi-GPU equal-nnz row slices (partition kernels.hpp:124-129).
+__global__ void row_slices_kernel(const int* __restrict__ rp, int m, long long nnz,
+                                  long long parts, long long* __restrict__ bounds) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g > parts) return;
+  if (g == 0) { bounds[0] = 0; return; }
+  if (g == parts) { bounds[parts] = m; return; }
+  const long long target = nnz * g / parts;
+  long long b = lower_bound_i32(rp, (long long)m + 1, target);
+  bounds[g] = b > m ? m : b;
+}
+
+// Zero the empty rows of Y (reference: Y zero-allocated, csr.hpp:66-72).
+__global__ void zero_rows_kernel(const int* __restrict__ erow, int ne, int N,
+                                 float* __restrict__ Y) {
+  const long long total = (long long)ne * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = erow[i / N];
+    __stcs(Y + r * N + (i % N), 0.f);
+  }
+}
+// All of Y zero (nnz == 0 or every row empty).
+__global__ void zero_all_kernel(float* __restrict__ Y, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    Y[i] = 0.f;
+}
+
+// Long-row fix-up: Y[r] = T[t1] + H[q0] + ... + H[q1] in ascending order
+// (the reference's serial boundary merge, kernels.hpp:316-323 / :448-453,
+// restricted to rows whose partials were not merged in registers).
+__global__ void fixup_kernel(const int* __restrict__ list, int nlong,
+                             const int* __restrict__ crp, const int* __restrict__ rid,
+                             const float* __restrict__ H, const float* __restrict__ Tsl,
+                             float* __restrict__ Y, int N, long long TS, long long CH) {
+  const long long T = TS / CH;
+  const long long total = (long long)nlong * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = list[i / N];
+    const int j = (int)(i % N);
+    const long long s = crp[c], f = crp[c + 1];
+    const long long t1 = s / TS;
+    const long long q0 = (t1 + 1) * T, q1 = (f - 1) / CH;
+    float acc = Tsl[t1 * N + j];
+    long long q = q0;
+    for (; q + 8 <= q1 + 1; q += 8) {
+      float h[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) h[u] = H[(q + u) * N + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, h[u]);
+    }
+    for (; q <= q1; ++q) acc = __fadd_rn(acc, H[q * N + j]);
+    Y[(long long)rid[c] * N + j] = acc;
+  }
+}
+
+// Row slice [r0, r1) rebased: rp_out[i] = rp[r0+i] - rp[r0].
+__global__ void rebase_kernel(const int* __restrict__ rp, long long r0, long long rows,
+                              int* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= rows;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = rp[r0 + i] - rp[r0];
+}
+
+}  // namespace spmk_dev

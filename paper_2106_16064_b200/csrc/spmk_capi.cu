@@ -1,0 +1,1038 @@
+// spmk_capi.cu — C ABI of the B200-native adaptive SpMV/SpMM engine.
+// See include/spmk_capi.h for the contract (reference interface per entry).
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/spmk_capi.h"
+#include "aux_kernels.cuh"
+#include "gen_kernels.cuh"
+#include "par_kernels.cuh"
+#include "seq_kernels.cuh"
+
+using namespace spmk_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+spmk_status fail(spmk_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+struct CudaError {
+  spmk_status st;
+  std::string msg;
+};
+
+#define CK(expr)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      throw CudaError{_e == cudaErrorMemoryAllocation ? SPMK_ENOMEM : SPMK_ECUDA,    \
+                      std::string(#expr) + ": " + cudaGetErrorString(_e)};           \
+  } while (0)
+
+int grid_for(long long n, int threads = 256, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+template <typename T>
+T* dev_alloc(size_t count) {
+  T* p = nullptr;
+  CK(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+  return p;
+}
+
+struct Plan {
+  int* rlo = nullptr;      // ntiles + 1
+  long long ntiles = 0;
+  long long TS = 0, CH = 0;
+  int* longrows = nullptr;
+  int nlong = 0;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct spmk_csr_s {
+  int device = 0;
+  long long m = 0, k = 0, nnz = 0;
+  int* rp = nullptr;
+  int* col = nullptr;
+  float* val = nullptr;
+  bool own_rp = true, own_col = true, own_val = true;
+  // resident row metadata
+  int mne = 0;            // non-empty rows
+  int* crp = nullptr;     // mne+1
+  int* rid = nullptr;     // mne
+  int nempty = 0;
+  int* erow = nullptr;    // nempty
+  long long max_row = 0;
+  unsigned long long sum_len2 = 0;
+  // caches
+  std::map<std::tuple<int, long long, long long>, Plan> plans;
+  float* scratch = nullptr;
+  size_t scratch_floats = 0;
+  float* stage_x = nullptr;
+  float* stage_y = nullptr;
+  size_t stage_x_n = 0, stage_y_n = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+void free_handle(spmk_csr_s* h) {
+  DeviceGuard g(h->device);
+  if (h->own_rp) cudaFree(h->rp);
+  if (h->own_col) cudaFree(h->col);
+  if (h->own_val) cudaFree(h->val);
+  cudaFree(h->crp);
+  cudaFree(h->rid);
+  cudaFree(h->erow);
+  for (auto& kv : h->plans) {
+    cudaFree(kv.second.rlo);
+    cudaFree(kv.second.longrows);
+  }
+  cudaFree(h->scratch);
+  cudaFree(h->stage_x);
+  cudaFree(h->stage_y);
+  delete h;
+}
+
+// Row metadata: non-empty compaction + moments (one-time, at create).
+void build_meta(spmk_csr_s* h, cudaStream_t s) {
+  const int m = (int)h->m;
+  h->crp = dev_alloc<int>((size_t)m + 1);
+  h->rid = dev_alloc<int>((size_t)m);
+  h->erow = dev_alloc<int>((size_t)m);
+  int* flag = dev_alloc<int>((size_t)m + 1);
+  int* pos = dev_alloc<int>((size_t)m + 1);
+  unsigned long long* mom = dev_alloc<unsigned long long>(4);
+  CK(cudaMemsetAsync(mom, 0, 4 * sizeof(unsigned long long), s));
+  if (m > 0) {
+    nonempty_flag_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, flag);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, pos, m + 1, s);
+    void* tmp = dev_alloc<char>(tmp_bytes);
+    CK(cudaMemsetAsync(flag + m, 0, sizeof(int), s));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, pos, m + 1, s);
+    compact_scatter_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, pos, h->crp, h->rid, h->erow);
+    row_moments_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, mom);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h->mne, pos + m, sizeof(int), cudaMemcpyDeviceToHost, s));
+    unsigned long long hm[4];
+    CK(cudaMemcpyAsync(hm, mom, sizeof(hm), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    h->sum_len2 = hm[1];
+    h->max_row = (long long)hm[2];
+    h->nempty = m - h->mne;
+  }
+  // crp[mne] = nnz
+  const int nnz32 = (int)h->nnz;
+  CK(cudaMemcpyAsync(h->crp + h->mne, &nnz32, sizeof(int), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(flag);
+  cudaFree(pos);
+  cudaFree(mom);
+}
+
+// Plan for a nonzero-split kernel: tiles of TS nonzeros made of CH-chunks.
+Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t s) {
+  auto key = std::make_tuple(kind, TS, CH);
+  auto it = h->plans.find(key);
+  if (it != h->plans.end()) return it->second;
+  Plan p;
+  p.TS = TS;
+  p.CH = CH;
+  p.ntiles = (h->nnz + TS - 1) / TS;
+  p.rlo = dev_alloc<int>((size_t)p.ntiles + 1);
+  tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo);
+  int* cnt = dev_alloc<int>(1);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+  // upper bound on long rows: nnz / (TS+1)
+  const long long cap = h->nnz / (TS + 1) + 1;
+  p.longrows = dev_alloc<int>((size_t)cap);
+  if (h->mne > 0)
+    long_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, TS, p.longrows, cnt);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&p.nlong, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(cnt);
+  return h->plans.emplace(key, p).first->second;
+}
+
+float* get_scratch(spmk_csr_s* h, size_t floats) {
+  if (floats > h->scratch_floats) {
+    cudaFree(h->scratch);
+    h->scratch = nullptr;
+    h->scratch_floats = 0;
+    h->scratch = dev_alloc<float>(floats);
+    h->scratch_floats = floats;
+  }
+  return h->scratch;
+}
+
+spmk_kernel_config cfg_or_default(const spmk_kernel_config* cfg) {
+  spmk_kernel_config c;
+  spmk_default_config(&c);
+  return cfg ? *cfg : c;
+}
+
+bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// ------------------------------------------------------------ seq launch
+template <int LPU, int CPL, bool VEC, int B, bool WS>
+void launch_seq_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
+  const int upb = 256 / LPU;
+  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
+  seq_kernel<LPU, CPL, VEC, B, WS><<<grid, 256, 0, s>>>(a);
+}
+
+template <bool WS>
+void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
+  const int N = a.N;
+  if (N >= 17) {
+    int cpl = N <= 32 ? 1 : (N <= 64 ? 2 : 4);
+    a.ncol_tile = 32 * cpl;
+    const int tiles = (N + a.ncol_tile - 1) / a.ncol_tile;
+    const bool vec = aligned && (N % cpl == 0);
+    if (cpl == 1) launch_seq_t<32, 1, false, 32, WS>(a, tiles, s);
+    else if (cpl == 2 && vec) launch_seq_t<32, 2, true, 16, WS>(a, tiles, s);
+    else if (cpl == 2) launch_seq_t<32, 2, false, 16, WS>(a, tiles, s);
+    else if (vec) launch_seq_t<32, 4, true, 8, WS>(a, tiles, s);
+    else launch_seq_t<32, 4, false, 8, WS>(a, tiles, s);
+  } else {
+    const int lpu = next_pow2(N);
+    a.ncol_tile = lpu;
+    switch (lpu) {
+      case 1: launch_seq_t<1, 1, false, 16, WS>(a, 1, s); break;
+      case 2: launch_seq_t<2, 1, false, 16, WS>(a, 1, s); break;
+      case 4: launch_seq_t<4, 1, false, 16, WS>(a, 1, s); break;
+      case 8: launch_seq_t<8, 1, false, 16, WS>(a, 1, s); break;
+      default: launch_seq_t<16, 1, false, 16, WS>(a, 1, s); break;
+    }
+  }
+}
+
+// ------------------------------------------------------------ par launch
+template <int W, int VL, int CT, bool V4>
+void launch_par_rs_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
+  constexpr int G = W / VL;
+  const long long groups_needed = a.mne;
+  const long long threads = groups_needed * G;
+  long long blocks = (threads + 255) / 256;
+  blocks = std::max(1LL, std::min(blocks, 148LL * 32));
+  par_rs_kernel<W, VL, CT, V4><<<dim3((unsigned)blocks, ncol_tiles), 256, 0, s>>>(a);
+}
+
+template <int W, int VL>
+void launch_par_rs_w(ParArgs a, bool aligned, cudaStream_t s) {
+  const int N = a.N;
+  int ct = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+  a.ncol_tile = ct;
+  const int tiles = (N + ct - 1) / ct;
+  const bool v4 = aligned && (N % 4 == 0) && ct >= 4;
+  switch (ct) {
+    case 1: launch_par_rs_t<W, VL, 1, false>(a, tiles, s); break;
+    case 2: launch_par_rs_t<W, VL, 2, false>(a, tiles, s); break;
+    case 4: v4 ? launch_par_rs_t<W, VL, 4, true>(a, tiles, s) : launch_par_rs_t<W, VL, 4, false>(a, tiles, s); break;
+    case 8: v4 ? launch_par_rs_t<W, VL, 8, true>(a, tiles, s) : launch_par_rs_t<W, VL, 8, false>(a, tiles, s); break;
+    case 16: v4 ? launch_par_rs_t<W, VL, 16, true>(a, tiles, s) : launch_par_rs_t<W, VL, 16, false>(a, tiles, s); break;
+    default: v4 ? launch_par_rs_t<W, VL, 32, true>(a, tiles, s) : launch_par_rs_t<W, VL, 32, false>(a, tiles, s); break;
+  }
+}
+
+void launch_par_rs(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
+  switch (W) {
+    case 2: launch_par_rs_w<2, 1>(a, aligned, s); break;
+    case 4: launch_par_rs_w<4, 1>(a, aligned, s); break;
+    case 8: launch_par_rs_w<8, 1>(a, aligned, s); break;
+    case 16: launch_par_rs_w<16, 1>(a, aligned, s); break;
+    case 32: launch_par_rs_w<32, 1>(a, aligned, s); break;
+    default: launch_par_rs_w<64, 2>(a, aligned, s); break;
+  }
+}
+
+template <int W, int CT>
+void launch_par_ws_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
+  const int upb = 256 / W;
+  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
+  par_ws_kernel<W, CT><<<grid, 256, 0, s>>>(a);
+}
+
+template <int W>
+void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
+  const int N = a.N;
+  int ct = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : 8;
+  (void)aligned;
+  a.ncol_tile = ct;
+  const int tiles = (N + ct - 1) / ct;
+  switch (ct) {
+    case 1: launch_par_ws_t<W, 1>(a, tiles, s); break;
+    case 2: launch_par_ws_t<W, 2>(a, tiles, s); break;
+    case 4: launch_par_ws_t<W, 4>(a, tiles, s); break;
+    default: launch_par_ws_t<W, 8>(a, tiles, s); break;
+  }
+}
+
+void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
+  switch (W) {
+    case 2: launch_par_ws_w<2>(a, aligned, s); break;
+    case 4: launch_par_ws_w<4>(a, aligned, s); break;
+    case 8: launch_par_ws_w<8>(a, aligned, s); break;
+    case 16: launch_par_ws_w<16>(a, aligned, s); break;
+    default: launch_par_ws_w<32>(a, aligned, s); break;
+  }
+}
+
+// Tiles: ~256 nonzeros per unit (any multiple of the chunk keeps exactness).
+long long tile_chunks(long long chunk) {
+  long long t = 256 / chunk;
+  return t < 1 ? 1 : t;
+}
+
+spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config& cfg,
+                     const float* d_x, int64_t n, float* d_y, cudaStream_t s) {
+  const long long M = h->m;
+  if (n == 0 || M == 0) return SPMK_OK;
+  if (h->nnz == 0 || h->mne == 0) {
+    zero_all_kernel<<<grid_for(M * n), 256, 0, s>>>(d_y, M * n);
+    CK(cudaGetLastError());
+    return SPMK_OK;
+  }
+  if (n > INT32_MAX / 2) return fail(SPMK_EUNSUPPORTED, "n too large");
+  const int N = (int)n;
+  const bool aligned = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
+  // empty rows -> 0 (the reference's zero-initialised Y)
+  if (h->nempty > 0)
+    zero_rows_kernel<<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y);
+
+  if (id == SPMK_SEQ_ROWSPLIT || id == SPMK_SEQ_BALANCED) {
+    SeqArgs a{};
+    a.crp = h->crp;
+    a.rid = h->rid;
+    a.col = h->col;
+    a.val = h->val;
+    a.X = d_x;
+    a.Y = d_y;
+    a.mne = h->mne;
+    a.nnz = (int)h->nnz;
+    a.N = N;
+    if (id == SPMK_SEQ_ROWSPLIT) {
+      const double avg = (double)h->nnz / (double)h->mne;
+      int rb = (int)std::lround(256.0 / std::max(avg, 1.0));
+      a.RB = std::max(1, std::min(rb, 256));
+      a.nunits = (h->mne + a.RB - 1) / a.RB;
+      launch_seq<false>(a, aligned, s);
+    } else {
+      const long long CH = (long long)cfg.seq_chunk;
+      const long long TS = CH * tile_chunks(CH);
+      Plan& p = get_plan(h, 1, TS, CH, s);
+      a.rlo = p.rlo;
+      a.TS = TS;
+      a.CH = CH;
+      a.nunits = (int)p.ntiles;
+      if (p.nlong > 0) {
+        const long long nch = (h->nnz + CH - 1) / CH;
+        float* sc = get_scratch(h, (size_t)(nch + p.ntiles) * N);
+        a.H = sc;
+        a.Tsl = sc + (size_t)nch * N;
+      }
+      launch_seq<true>(a, aligned, s);
+      if (p.nlong > 0)
+        fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
+            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH);
+    }
+  } else {
+    ParArgs a{};
+    a.crp = h->crp;
+    a.rid = h->rid;
+    a.col = h->col;
+    a.val = h->val;
+    a.X = d_x;
+    a.Y = d_y;
+    a.mne = h->mne;
+    a.nnz = (int)h->nnz;
+    a.N = N;
+    const int W = (int)cfg.lane_width;
+    if (id == SPMK_PAR_ROWSPLIT) {
+      launch_par_rs(a, W, aligned, s);
+    } else {
+      if (W > 32) return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
+      const long long CH = W;
+      const long long TS = CH * tile_chunks(CH);
+      Plan& p = get_plan(h, 2, TS, CH, s);
+      a.rlo = p.rlo;
+      a.TS = TS;
+      a.nunits = (int)p.ntiles;
+      if (p.nlong > 0) {
+        const long long nch = (h->nnz + CH - 1) / CH;
+        float* sc = get_scratch(h, (size_t)(nch + p.ntiles) * N);
+        a.H = sc;
+        a.Tsl = sc + (size_t)nch * N;
+      }
+      launch_par_ws(a, W, aligned, s);
+      if (p.nlong > 0)
+        fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
+            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH);
+    }
+  }
+  CK(cudaGetLastError());
+  return SPMK_OK;
+}
+
+spmk_status create_from_device32(long long m, long long k, long long nnz, int* rp, int* col,
+                                 float* val, bool own, int device, spmk_csr_t* out,
+                                 cudaStream_t s) {
+  auto* h = new spmk_csr_s;
+  h->device = device;
+  h->m = m;
+  h->k = k;
+  h->nnz = nnz;
+  h->rp = rp;
+  h->col = col;
+  h->val = val;
+  h->own_rp = h->own_col = h->own_val = own;
+  try {
+    int* err = dev_alloc<int>(1);
+    CK(cudaMemsetAsync(err, 0, sizeof(int), s));
+    validate_kernel<<<grid_for(std::max(m, 1LL)), 256, 0, s>>>(rp, col, (int)m, (int)k, nnz, err);
+    CK(cudaGetLastError());
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(err);
+    if (herr) {
+      free_handle(h);
+      return fail(SPMK_EINVAL, (herr & 1) ? "row_ptr malformed (csr.hpp:95-119)"
+                               : (herr & 2) ? "column index out of range"
+                                            : "columns not strictly increasing within a row");
+    }
+    build_meta(h, s);
+  } catch (const CudaError& e) {
+    free_handle(h);
+    return fail(e.st, e.msg);
+  }
+  *out = h;
+  return SPMK_OK;
+}
+
+}  // namespace
+
+// =============================================================== C ABI
+extern "C" {
+
+const char* spmk_last_error(void) { return g_err.c_str(); }
+int spmk_version(void) { return SPMK_CAPI_VERSION; }
+
+void spmk_default_config(spmk_kernel_config* cfg) {
+  cfg->lane_width = 32;
+  cfg->vdl_group = 0;
+  cfg->seq_chunk = 256;
+  cfg->worker_count = 0;
+}
+void spmk_default_thresholds(spmk_thresholds* t) {
+  t->n_parallel_max = 4;
+  t->t_parallel_avg = 32.0;
+  t->t_cv = 1.0;
+}
+
+spmk_status spmk_check_config(const spmk_kernel_config* cfg) {
+  if (!cfg) return SPMK_OK;
+  if (!is_pow2(cfg->lane_width) || cfg->lane_width < 2 || cfg->lane_width > 64)
+    return fail(SPMK_EINVAL, "lane_width must be a power of two in [2, 64]");
+  if (cfg->vdl_group != 0 && cfg->vdl_group != 1 && cfg->vdl_group != 2 && cfg->vdl_group != 4)
+    return fail(SPMK_EINVAL, "vdl_group must be 0 (auto), 1, 2 or 4");
+  if (cfg->seq_chunk < 1) return fail(SPMK_EINVAL, "seq_chunk must be >= 1");
+  if (cfg->seq_chunk > (1ull << 30)) return fail(SPMK_EUNSUPPORTED, "seq_chunk too large for the device path");
+  return SPMK_OK;
+}
+
+const char* spmk_kernel_name(spmk_kernel_id id) {
+  switch (id) {
+    case SPMK_PAR_ROWSPLIT: return "par-rs";
+    case SPMK_PAR_BALANCED: return "par-ws";
+    case SPMK_SEQ_ROWSPLIT: return "seq-rs";
+    default: return "seq-ws";
+  }
+}
+
+spmk_status spmk_parse_kernel(const char* name, spmk_kernel_id* out) {
+  for (int i = 0; i < 4; ++i) {
+    if (std::strcmp(name, spmk_kernel_name((spmk_kernel_id)i)) == 0) {
+      *out = (spmk_kernel_id)i;
+      return SPMK_OK;
+    }
+  }
+  return fail(SPMK_EINVAL, std::string("unknown kernel name: ") + name);
+}
+
+spmk_status spmk_csr_create(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                            const int64_t* row_ptr, const int64_t* col_idx,
+                            const float* values, int device, spmk_csr_t* out) {
+  if (!out || !row_ptr || (nnz > 0 && (!col_idx || !values)))
+    return fail(SPMK_EINVAL, "null argument");
+  if (num_rows < 0 || num_cols < 0 || nnz < 0) return fail(SPMK_EINVAL, "negative dimension");
+  if (num_rows >= INT32_MAX || num_cols >= INT32_MAX || nnz >= INT32_MAX)
+    return fail(SPMK_EUNSUPPORTED, "device path narrows indices to int32 (need < 2^31)");
+  if (row_ptr[0] != 0 || row_ptr[num_rows] != nnz)
+    return fail(SPMK_EINVAL, "row_ptr[0] must be 0 and row_ptr[M] must equal nnz");
+  DeviceGuard g(device);
+  cudaStream_t s = nullptr;
+  int *rp = nullptr, *col = nullptr;
+  float* val = nullptr;
+  long long* tmp = nullptr;
+  int* bad = nullptr;
+  try {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    rp = dev_alloc<int>((size_t)num_rows + 1);
+    col = dev_alloc<int>((size_t)nnz);
+    val = dev_alloc<float>((size_t)nnz);
+    const long long chunk = 1LL << 24;
+    tmp = dev_alloc<long long>((size_t)std::min<long long>(chunk, std::max<long long>(nnz, num_rows + 1)));
+    bad = dev_alloc<int>(1);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    auto narrow = [&](const int64_t* src, int* dst, long long n) {
+      for (long long o = 0; o < n; o += chunk) {
+        const long long c = std::min(chunk, n - o);
+        CK(cudaMemcpyAsync(tmp, src + o, c * 8, cudaMemcpyHostToDevice, s));
+        narrow_kernel<<<grid_for(c), 256, 0, s>>>(tmp, dst + o, c, bad);
+        CK(cudaGetLastError());
+      }
+    };
+    narrow(row_ptr, rp, num_rows + 1);
+    narrow(col_idx, col, nnz);
+    if (nnz) CK(cudaMemcpyAsync(val, values, nnz * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    int hbad = 0;
+    CK(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+    cudaFree(bad);
+    tmp = nullptr;
+    bad = nullptr;
+    if (hbad) {
+      cudaFree(rp);
+      cudaFree(col);
+      cudaFree(val);
+      cudaStreamDestroy(s);
+      return fail(SPMK_EINVAL, "index out of int32 range");
+    }
+    spmk_status st = create_from_device32(num_rows, num_cols, nnz, rp, col, val, true, device, out, s);
+    cudaStreamDestroy(s);
+    return st;
+  } catch (const CudaError& e) {
+    cudaFree(rp);
+    cudaFree(col);
+    cudaFree(val);
+    cudaFree(tmp);
+    cudaFree(bad);
+    if (s) cudaStreamDestroy(s);
+    return fail(e.st, e.msg);
+  }
+}
+
+spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                                   const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                                   const float* d_values, int copy, spmk_csr_t* out) {
+  if (!out || !d_row_ptr) return fail(SPMK_EINVAL, "null argument");
+  if (num_rows < 0 || num_cols < 0 || nnz < 0) return fail(SPMK_EINVAL, "negative dimension");
+  if (num_rows >= INT32_MAX || num_cols >= INT32_MAX || nnz >= INT32_MAX)
+    return fail(SPMK_EUNSUPPORTED, "device path needs indices < 2^31");
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, d_row_ptr) != cudaSuccess || attr.type != cudaMemoryTypeDevice)
+    return fail(SPMK_EINVAL, "d_row_ptr is not device memory");
+  const int device = attr.device;
+  DeviceGuard g(device);
+  cudaStream_t s = nullptr;
+  try {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int* rp = const_cast<int*>(d_row_ptr);
+    int* col = const_cast<int*>(d_col_idx);
+    float* val = const_cast<float*>(d_values);
+    if (copy) {
+      rp = dev_alloc<int>((size_t)num_rows + 1);
+      col = dev_alloc<int>((size_t)nnz);
+      val = dev_alloc<float>((size_t)nnz);
+      CK(cudaMemcpyAsync(rp, d_row_ptr, (num_rows + 1) * 4, cudaMemcpyDeviceToDevice, s));
+      if (nnz) {
+        CK(cudaMemcpyAsync(col, d_col_idx, nnz * 4, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(val, d_values, nnz * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    spmk_status st = create_from_device32(num_rows, num_cols, nnz, rp, col, val, copy != 0,
+                                          device, out, s);
+    cudaStreamDestroy(s);
+    return st;
+  } catch (const CudaError& e) {
+    if (s) cudaStreamDestroy(s);
+    return fail(e.st, e.msg);
+  }
+}
+
+spmk_status spmk_csr_slice(spmk_csr_t a, int64_t row_begin, int64_t row_end, int device,
+                           spmk_csr_t* out) {
+  if (!a || !out || row_begin < 0 || row_end < row_begin || row_end > a->m)
+    return fail(SPMK_EINVAL, "bad slice");
+  try {
+    int rp_b = 0, rp_e = 0;
+    {
+      DeviceGuard g(a->device);
+      CK(cudaMemcpy(&rp_b, a->rp + row_begin, 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&rp_e, a->rp + row_end, 4, cudaMemcpyDeviceToHost));
+    }
+    const long long rows = row_end - row_begin, nnz = rp_e - rp_b;
+    DeviceGuard g(device);
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int* rp = dev_alloc<int>((size_t)rows + 1);
+    int* col = dev_alloc<int>((size_t)nnz);
+    float* val = dev_alloc<float>((size_t)nnz);
+    int* rpsrc = a->rp;
+    int* tmp = nullptr;
+    if (device != a->device) {
+      tmp = dev_alloc<int>((size_t)rows + 1);
+      CK(cudaMemcpyPeerAsync(tmp, device, a->rp + row_begin, a->device, (rows + 1) * 4, s));
+      CK(cudaMemcpyPeerAsync(col, device, a->col + rp_b, a->device, nnz * 4, s));
+      CK(cudaMemcpyPeerAsync(val, device, a->val + rp_b, a->device, nnz * 4, s));
+      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(tmp, 0, rows, rp);
+    } else {
+      CK(cudaMemcpyAsync(col, a->col + rp_b, nnz * 4, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(val, a->val + rp_b, nnz * 4, cudaMemcpyDeviceToDevice, s));
+      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(rpsrc, row_begin, rows, rp);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    if (tmp) cudaFree(tmp);
+    spmk_status st = create_from_device32(rows, a->k, nnz, rp, col, val, true, device, out, s);
+    cudaStreamDestroy(s);
+    return st;
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+}
+
+spmk_status spmk_csr_destroy(spmk_csr_t a) {
+  if (a) free_handle(a);
+  return SPMK_OK;
+}
+
+spmk_status spmk_csr_info(spmk_csr_t a, int64_t* num_rows, int64_t* num_cols, int64_t* nnz,
+                          int64_t* max_row_nnz, int64_t* empty_rows) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  if (num_rows) *num_rows = a->m;
+  if (num_cols) *num_cols = a->k;
+  if (nnz) *nnz = a->nnz;
+  if (max_row_nnz) *max_row_nnz = a->max_row;
+  if (empty_rows) *empty_rows = a->nempty;
+  return SPMK_OK;
+}
+
+spmk_status spmk_csr_device_arrays(spmk_csr_t a, const int32_t** d_row_ptr,
+                                   const int32_t** d_col_idx, const float** d_values) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  if (d_row_ptr) *d_row_ptr = a->rp;
+  if (d_col_idx) *d_col_idx = a->col;
+  if (d_values) *d_values = a->val;
+  return SPMK_OK;
+}
+
+spmk_status spmk_csr_download(spmk_csr_t a, int64_t* row_ptr, int64_t* col_idx, float* values) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  DeviceGuard g(a->device);
+  try {
+    auto widen = [&](const int* src, int64_t* dst, long long n) {
+      if (!dst || n == 0) return;
+      long long* tmp = dev_alloc<long long>((size_t)n);
+      widen_kernel<<<grid_for(n), 256>>>(src, tmp, n);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(dst, tmp, n * 8, cudaMemcpyDeviceToHost));
+      cudaFree(tmp);
+    };
+    widen(a->rp, row_ptr, a->m + 1);
+    widen(a->col, col_idx, a->nnz);
+    if (values && a->nnz) CK(cudaMemcpy(values, a->val, a->nnz * 4, cudaMemcpyDeviceToHost));
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+// csr.hpp:166-181, sequential double sum (the reference order).
+spmk_status spmk_features_host(int64_t num_rows, const int64_t* row_ptr, spmk_features* out) {
+  if (num_rows < 1) return fail(SPMK_EINVAL, "extract_features requires num_rows >= 1");
+  const long long nnz = row_ptr[num_rows];
+  out->num_rows = num_rows;
+  out->nnz = nnz;
+  out->avg_row = (double)nnz / (double)num_rows;
+  double ss = 0.0;
+  for (long long i = 0; i < num_rows; ++i) {
+    const double d = (double)(row_ptr[i + 1] - row_ptr[i]) - out->avg_row;
+    ss += d * d;
+  }
+  out->stdv_row = std::sqrt(ss / (double)num_rows);
+  out->cv = out->avg_row == 0.0 ? 0.0 : out->stdv_row / out->avg_row;
+  return SPMK_OK;
+}
+
+spmk_status spmk_features_compute(spmk_csr_t a, spmk_features* out) {
+  if (!a || !out) return fail(SPMK_EINVAL, "null argument");
+  if (a->m < 1) return fail(SPMK_EINVAL, "extract_features requires num_rows >= 1");
+  // exact integer moments (computed at create); host finalize
+  const long double m = (long double)a->m, nnz = (long double)a->nnz;
+  out->num_rows = a->m;
+  out->nnz = a->nnz;
+  out->avg_row = (double)a->nnz / (double)a->m;  // bit-identical to csr.hpp:170
+  long double ss = (long double)a->sum_len2 - nnz * nnz / m;
+  if (ss < 0) ss = 0;
+  out->stdv_row = (double)std::sqrt(ss / m);
+  out->cv = out->avg_row == 0.0 ? 0.0 : out->stdv_row / out->avg_row;
+  return SPMK_OK;
+}
+
+spmk_kernel_id spmk_select(const spmk_features* f, uint64_t n, const spmk_thresholds* t) {
+  spmk_thresholds d;
+  spmk_default_thresholds(&d);
+  const spmk_thresholds& th = t ? *t : d;
+  if (n <= th.n_parallel_max) return f->avg_row < th.t_parallel_avg ? SPMK_PAR_BALANCED : SPMK_PAR_ROWSPLIT;
+  return f->cv > th.t_cv ? SPMK_SEQ_BALANCED : SPMK_SEQ_ROWSPLIT;
+}
+
+spmk_status spmk_select_for(spmk_csr_t a, uint64_t n, const spmk_thresholds* t,
+                            spmk_kernel_id* out) {
+  spmk_features f;
+  spmk_status st = spmk_features_compute(a, &f);
+  if (st != SPMK_OK) return st;
+  spmk_thresholds d;
+  spmk_default_thresholds(&d);
+  const spmk_thresholds& th = t ? *t : d;
+  // tie-guard: near a threshold recompute in the reference's exact order
+  if (std::fabs(f.cv - th.t_cv) <= 1e-9 * std::fabs(th.t_cv)) {
+    std::vector<int64_t> rp((size_t)a->m + 1);
+    st = spmk_csr_download(a, rp.data(), nullptr, nullptr);
+    if (st != SPMK_OK) return st;
+    spmk_features_host(a->m, rp.data(), &f);
+  }
+  *out = spmk_select(&f, n, &th);
+  return SPMK_OK;
+}
+
+spmk_status spmk_plan(spmk_csr_t a, int64_t chunk, int64_t* chunk_first_row, int64_t* num_chunks) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  if (chunk < 1) return fail(SPMK_EINVAL, "chunk_size must be >= 1");
+  const long long nch = (a->nnz + chunk - 1) / chunk;
+  if (num_chunks) *num_chunks = nch;
+  if (!chunk_first_row || nch == 0) return SPMK_OK;
+  DeviceGuard g(a->device);
+  try {
+    long long* d = dev_alloc<long long>((size_t)nch);
+    chunk_first_row_kernel<<<grid_for(nch), 256>>>(a->rp, (int)a->m, nch, chunk, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(chunk_first_row, d, nch * 8, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+spmk_status spmk_plan_elem_row(spmk_csr_t a, int64_t* elem_row) {
+  if (!a || !elem_row) return fail(SPMK_EINVAL, "null argument");
+  if (a->nnz == 0) return SPMK_OK;
+  DeviceGuard g(a->device);
+  try {
+    long long* d = dev_alloc<long long>((size_t)a->nnz);
+    elem_row_kernel<<<grid_for(a->nnz), 256>>>(a->rp, (int)a->m, a->nnz, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(elem_row, d, a->nnz * 8, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+void spmk_partition(int64_t items, int64_t parts, int64_t w, int64_t* lo, int64_t* hi) {
+  *lo = items * w / parts;
+  *hi = items * (w + 1) / parts;
+}
+
+spmk_status spmk_row_slices(spmk_csr_t a, int64_t parts, int64_t* bounds) {
+  if (!a || !bounds || parts < 1) return fail(SPMK_EINVAL, "bad argument");
+  DeviceGuard g(a->device);
+  try {
+    long long* d = dev_alloc<long long>((size_t)parts + 1);
+    row_slices_kernel<<<grid_for(parts + 1), 256>>>(a->rp, (int)a->m, a->nnz, parts, d);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(bounds, d, (parts + 1) * 8, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int64_t g2 = 1; g2 <= parts; ++g2)
+      if (bounds[g2] < bounds[g2 - 1]) bounds[g2] = bounds[g2 - 1];
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+spmk_status spmk_spmm(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg,
+                      const float* d_x, int64_t n, float* d_y, void* stream) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  if ((int)id < 0 || (int)id > 3) return fail(SPMK_EINVAL, "bad kernel id");
+  spmk_status st = spmk_check_config(cfg);
+  if (st != SPMK_OK) return st;
+  if (n < 0) return fail(SPMK_EDIM, "negative n");
+  if (n > 0 && a->m > 0 && !d_y) return fail(SPMK_EINVAL, "null Y");
+  if (n > 0 && a->k > 0 && !d_x) return fail(SPMK_EINVAL, "null X");
+  const spmk_kernel_config c = cfg_or_default(cfg);
+  std::lock_guard<std::mutex> lk(a->mu);
+  DeviceGuard g(a->device);
+  try {
+    return run_spmm(a, id, c, d_x, n, d_y, (cudaStream_t)stream);
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+}
+
+spmk_status spmk_spmm_auto(spmk_csr_t a, const spmk_thresholds* t, const spmk_kernel_config* cfg,
+                           const float* d_x, int64_t n, float* d_y, void* stream,
+                           spmk_kernel_id* chosen) {
+  spmk_kernel_id id;
+  spmk_status st = spmk_select_for(a, (uint64_t)n, t, &id);
+  if (st != SPMK_OK) return st;
+  if (chosen) *chosen = id;
+  return spmk_spmm(a, id, cfg, d_x, n, d_y, stream);
+}
+
+spmk_status spmk_spmm_host(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg,
+                           const float* x, int64_t n, float* y, void* stream) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  spmk_status st = spmk_check_config(cfg);
+  if (st != SPMK_OK) return st;
+  if (n < 0) return fail(SPMK_EDIM, "negative n");
+  if (n == 0 || a->m == 0) return SPMK_OK;
+  const spmk_kernel_config c = cfg_or_default(cfg);
+  std::lock_guard<std::mutex> lk(a->mu);
+  DeviceGuard g(a->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    const size_t nx = (size_t)a->k * n, ny = (size_t)a->m * n;
+    if (nx > a->stage_x_n) {
+      cudaFree(a->stage_x);
+      a->stage_x = nullptr;
+      a->stage_x_n = 0;
+      a->stage_x = dev_alloc<float>(nx);
+      a->stage_x_n = nx;
+    }
+    if (ny > a->stage_y_n) {
+      cudaFree(a->stage_y);
+      a->stage_y = nullptr;
+      a->stage_y_n = 0;
+      a->stage_y = dev_alloc<float>(ny);
+      a->stage_y_n = ny;
+    }
+    if (nx) CK(cudaMemcpyAsync(a->stage_x, x, nx * 4, cudaMemcpyHostToDevice, s));
+    st = run_spmm(a, id, c, a->stage_x, n, a->stage_y, s);
+    if (st != SPMK_OK) return st;
+    CK(cudaMemcpyAsync(y, a->stage_y, ny * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+spmk_status spmk_spmm_csr_host(int64_t num_rows, int64_t num_cols, int64_t nnz,
+                               const int64_t* row_ptr, const int64_t* col_idx,
+                               const float* values, spmk_kernel_id id,
+                               const spmk_kernel_config* cfg, const float* x, int64_t n,
+                               float* y, int device) {
+  spmk_status st = spmk_check_config(cfg);
+  if (st != SPMK_OK) return st;
+  spmk_csr_t h = nullptr;
+  st = spmk_csr_create(num_rows, num_cols, nnz, row_ptr, col_idx, values, device, &h);
+  if (st != SPMK_OK) return st;
+  st = spmk_spmm_host(h, id, cfg, x, n, y, nullptr);
+  spmk_csr_destroy(h);
+  return st;
+}
+
+spmk_status spmk_kernel_stats(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg,
+                              int64_t n, uint64_t* lane_multiplies, uint64_t* scan_ops) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  spmk_status st = spmk_check_config(cfg);
+  if (st != SPMK_OK) return st;
+  const spmk_kernel_config c = cfg_or_default(cfg);
+  *lane_multiplies = 0;
+  *scan_ops = 0;
+  if (n == 0 || id == SPMK_SEQ_ROWSPLIT || id == SPMK_SEQ_BALANCED) return SPMK_OK;
+  const uint64_t w = c.lane_width;
+  uint64_t levels = 0;
+  for (uint64_t off = 1; off < w; off <<= 1) ++levels;
+  int64_t group = c.vdl_group ? (int64_t)c.vdl_group : (n >= 4 ? 4 : n >= 2 ? 2 : 1);
+  if (group > n) group = n;
+  const uint64_t wc_sum = (uint64_t)((n / group) * group + (n % group));
+  if (id == SPMK_PAR_ROWSPLIT) {
+    // sum over non-empty rows of ceil(len/W) * W (kernels.hpp:187)
+    std::vector<int64_t> rp((size_t)a->m + 1);
+    st = spmk_csr_download(a, rp.data(), nullptr, nullptr);
+    if (st != SPMK_OK) return st;
+    uint64_t lm = 0, rows = 0;
+    for (int64_t i = 0; i < a->m; ++i) {
+      const uint64_t len = (uint64_t)(rp[i + 1] - rp[i]);
+      if (!len) continue;
+      lm += (len + w - 1) / w * w;
+      ++rows;
+    }
+    *lane_multiplies = lm * wc_sum;
+    *scan_ops = rows * levels * w * wc_sum;
+  } else {
+    if (a->nnz == 0) return SPMK_OK;
+    const uint64_t chunks = ((uint64_t)a->nnz + w - 1) / w;
+    *lane_multiplies = chunks * w * wc_sum;
+    *scan_ops = chunks * levels * w * wc_sum;
+  }
+  return SPMK_OK;
+}
+
+double spmk_kernel_tolerance(int64_t max_row_nnz) {
+  return 1e-5 * std::log2((double)max_row_nnz + 2.0);
+}
+
+spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes) {
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaStreamAttrValue attr;
+    std::memset(&attr, 0, sizeof(attr));
+    if (bytes == 0 || d_x == nullptr) {
+      attr.accessPolicyWindow.num_bytes = 0;
+      CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
+      CK(cudaCtxResetPersistingL2Cache());
+      return SPMK_OK;
+    }
+    int max_win = 0, max_persist = 0;
+    CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    if (max_win <= 0 || max_persist <= 0) return fail(SPMK_EUNSUPPORTED, "no L2 persistence");
+    const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
+    CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+    const size_t win = std::min<size_t>(bytes, (size_t)max_win);
+    attr.accessPolicyWindow.base_ptr = const_cast<float*>(d_x);
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)persist / (float)win);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+spmk_status spmk_make_dense(int64_t rows, int64_t cols, uint64_t seed, float* d_out, void* stream) {
+  const long long total = rows * cols;
+  if (total <= 0) return SPMK_OK;
+  make_dense_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(d_out, total, seed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SPMK_ECUDA, cudaGetErrorString(e));
+  return SPMK_OK;
+}
+
+spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, double b, double c,
+                               double d, uint64_t seed, int device, spmk_csr_t* out) {
+  // rmat.hpp:46-59 validate
+  if (scale < 1 || scale > 30) return fail(SPMK_EINVAL, "rmat scale must be in [1, 30]");
+  if (edge_factor < 1) return fail(SPMK_EINVAL, "rmat edge_factor must be >= 1");
+  const double pr[4] = {a, b, c, d};
+  double sum = 0.0;
+  for (double q : pr) {
+    if (q < 0.0 || q > 1.0) return fail(SPMK_EINVAL, "rmat quadrant probability outside [0, 1]");
+    sum += q;
+  }
+  if (std::abs(sum - 1.0) > 1e-9) return fail(SPMK_EINVAL, "rmat quadrant probabilities must sum to 1");
+  if (scale > 30 || (edge_factor << scale) >= (1ull << 31))
+    return fail(SPMK_EUNSUPPORTED, "edge count must be < 2^31 on the device path");
+  DeviceGuard g(device);
+  const long long m = 1LL << scale;
+  const long long edges = (long long)(edge_factor << scale);
+  const double t_a = a, t_ab = a + b, t_abc = a + b + c;  // rmat.hpp:66-68
+  cudaStream_t s = nullptr;
+  try {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    unsigned long long* keys = dev_alloc<unsigned long long>((size_t)edges);
+    unsigned long long* sorted = dev_alloc<unsigned long long>((size_t)edges);
+    rmat_edges_kernel<<<grid_for(edges, 256, 148 * 64), 256, 0, s>>>(keys, edges, (int)scale, seed,
+                                                                     t_a, t_ab, t_abc);
+    CK(cudaGetLastError());
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, edges, 0, 2 * (int)scale, s);
+    void* tmp = dev_alloc<char>(tb);
+    cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, edges, 0, 2 * (int)scale, s);
+    cudaFree(tmp);
+    int* flag = reinterpret_cast<int*>(keys);  // reuse: edges*8 bytes >= 2*edges ints
+    int* pos = flag + edges;
+    unique_flag_kernel<<<grid_for(edges), 256, 0, s>>>(sorted, edges, flag);
+    size_t sb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, sb, flag, pos, edges, s);
+    tmp = dev_alloc<char>(sb);
+    cub::DeviceScan::ExclusiveSum(tmp, sb, flag, pos, edges, s);
+    int last_flag = 0, last_pos = 0;
+    CK(cudaMemcpyAsync(&last_flag, flag + edges - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&last_pos, pos + edges - 1, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    const long long nnz = (long long)last_pos + last_flag;
+    int* col = dev_alloc<int>((size_t)nnz);
+    float* val = dev_alloc<float>((size_t)nnz);
+    unsigned long long* rows = dev_alloc<unsigned long long>((size_t)nnz);
+    unique_scatter_kernel<<<grid_for(edges), 256, 0, s>>>(sorted, edges, flag, pos, (int)scale, col,
+                                                           val, rows);
+    cudaFree(keys);
+    cudaFree(sorted);
+    int* rp = dev_alloc<int>((size_t)m + 1);
+    rowptr_from_rows_kernel<<<grid_for(m + 1), 256, 0, s>>>(rows, nnz, m, rp);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    cudaFree(rows);
+    spmk_status st = create_from_device32(m, m, nnz, rp, col, val, true, device, out, s);
+    cudaStreamDestroy(s);
+    return st;
+  } catch (const CudaError& e) {
+    if (s) cudaStreamDestroy(s);
+    return fail(e.st, e.msg);
+  }
+}
+
+}  // extern "C"
