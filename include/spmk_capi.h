@@ -195,6 +195,15 @@ double spmk_kernel_tolerance(int64_t max_row_nnz);
  * device's max window / persisting-L2 size.  bytes=0 clears the window. */
 spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes);
 
+/* ------------------------------------------------------------ measurement */
+/* Kernel launches issued by this library since load (all entry points). */
+uint64_t spmk_launch_count(void);
+/* When enabled, spmk_spmm records CUDA events on its stream around the
+ * dominant (variant) kernel and around the whole call; spmk_timing_last
+ * synchronizes on them and returns milliseconds.  For bench.py's roofline. */
+spmk_status spmk_timing_enable(int on);
+spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms);
+
 /* ------------------------------------------------------------ generators */
 /* generate_rmat<float> (rmat.hpp:61-88 + csr.hpp:123-164) on the device,
  * bit-identical to the reference (counter form of SplitMix64): returns a

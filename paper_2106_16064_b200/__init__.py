@@ -25,6 +25,9 @@ from .spmk import (  # noqa: F401
     kernel_name,
     kernel_tolerance,
     l2_persist_x,
+    launch_count,
+    timing_enable,
+    timing_last,
     load_library,
     make_dense_device,
     parse_kernel,

@@ -66,12 +66,15 @@ __device__ __forceinline__ unsigned group_mask() {
     return ((1u << LPU) - 1u) << ((threadIdx.x & 31) & ~(LPU - 1));
   }
 }
+// Group broadcast.  Callers keep the whole warp converged (warp-uniform loop
+// trip counts), so the shuffle uses the full mask: a runtime group mask makes
+// nvcc wrap every shuffle in a MATCH/REDUX convergence sequence.
 template <int LPU, typename T>
 __device__ __forceinline__ T gshfl(T v, int src) {
   if constexpr (LPU == 1) {
     return v;
   } else {
-    return __shfl_sync(group_mask<LPU>(), v, src, LPU);
+    return __shfl_sync(0xffffffffu, v, src, LPU);
   }
 }
 

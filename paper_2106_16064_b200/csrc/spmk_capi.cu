@@ -5,8 +5,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -65,6 +67,29 @@ struct Plan {
   int* longrows = nullptr;
   int nlong = 0;
 };
+
+std::atomic<uint64_t> g_launches{0};
+#define LAUNCHED(n) g_launches.fetch_add((n), std::memory_order_relaxed)
+
+struct Timing {
+  bool on = false;
+  int device = -1;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // call0, main0, main1, call1
+};
+thread_local Timing g_timing;
+
+void timing_record(int which, cudaStream_t s) {
+  if (!g_timing.on) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (g_timing.device != dev) {
+    for (auto& e : g_timing.ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : g_timing.ev) cudaEventCreate(&e);
+    g_timing.device = dev;
+  }
+  cudaEventRecord(g_timing.ev[which], s);
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -135,14 +160,14 @@ void build_meta(spmk_csr_s* h, cudaStream_t s) {
   unsigned long long* mom = dev_alloc<unsigned long long>(4);
   CK(cudaMemsetAsync(mom, 0, 4 * sizeof(unsigned long long), s));
   if (m > 0) {
-    nonempty_flag_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, flag);
+    nonempty_flag_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, flag); LAUNCHED(1);
     size_t tmp_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, pos, m + 1, s);
     void* tmp = dev_alloc<char>(tmp_bytes);
     CK(cudaMemsetAsync(flag + m, 0, sizeof(int), s));
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, pos, m + 1, s);
-    compact_scatter_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, pos, h->crp, h->rid, h->erow);
-    row_moments_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, mom);
+    compact_scatter_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, pos, h->crp, h->rid, h->erow); LAUNCHED(1);
+    row_moments_kernel<<<grid_for(m), 256, 0, s>>>(h->rp, m, mom); LAUNCHED(1);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(&h->mne, pos + m, sizeof(int), cudaMemcpyDeviceToHost, s));
     unsigned long long hm[4];
@@ -172,14 +197,14 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t
   p.CH = CH;
   p.ntiles = (h->nnz + TS - 1) / TS;
   p.rlo = dev_alloc<int>((size_t)p.ntiles + 1);
-  tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo);
+  tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo); LAUNCHED(1);
   int* cnt = dev_alloc<int>(1);
   CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
   // upper bound on long rows: nnz / (TS+1)
   const long long cap = h->nnz / (TS + 1) + 1;
   p.longrows = dev_alloc<int>((size_t)cap);
   if (h->mne > 0)
-    long_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, TS, p.longrows, cnt);
+    long_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, TS, p.longrows, cnt); LAUNCHED(1);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&p.nlong, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -217,32 +242,45 @@ template <int LPU, int CPL, bool VEC, int B, bool WS>
 void launch_seq_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   const int upb = 256 / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq_kernel<LPU, CPL, VEC, B, WS><<<grid, 256, 0, s>>>(a);
+  seq_kernel<LPU, CPL, VEC, B, WS><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
+}
+
+// Column mapping of the sequential sweep: a group of LPU lanes covers one
+// column tile; each lane owns CPL columns (float4/float2 when aligned), so
+// one warp instruction serves 32/LPU work units at once.
+template <bool WS, int CPL, bool VEC, int B>
+void launch_seq_lpu(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+  switch (lpu) {
+    case 1: launch_seq_t<1, CPL, VEC, B, WS>(a, tiles, s); break;
+    case 2: launch_seq_t<2, CPL, VEC, B, WS>(a, tiles, s); break;
+    case 4: launch_seq_t<4, CPL, VEC, B, WS>(a, tiles, s); break;
+    case 8: launch_seq_t<8, CPL, VEC, B, WS>(a, tiles, s); break;
+    case 16: launch_seq_t<16, CPL, VEC, B, WS>(a, tiles, s); break;
+    default: launch_seq_t<32, CPL, VEC, B, WS>(a, tiles, s); break;
+  }
 }
 
 template <bool WS>
 void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
   const int N = a.N;
-  if (N >= 17) {
-    int cpl = N <= 32 ? 1 : (N <= 64 ? 2 : 4);
-    a.ncol_tile = 32 * cpl;
-    const int tiles = (N + a.ncol_tile - 1) / a.ncol_tile;
-    const bool vec = aligned && (N % cpl == 0);
-    if (cpl == 1) launch_seq_t<32, 1, false, 32, WS>(a, tiles, s);
-    else if (cpl == 2 && vec) launch_seq_t<32, 2, true, 16, WS>(a, tiles, s);
-    else if (cpl == 2) launch_seq_t<32, 2, false, 16, WS>(a, tiles, s);
-    else if (vec) launch_seq_t<32, 4, true, 8, WS>(a, tiles, s);
-    else launch_seq_t<32, 4, false, 8, WS>(a, tiles, s);
-  } else {
+  if (aligned && N % 4 == 0) {
+    const int lpu = std::min(32, next_pow2(N / 4));
+    a.ncol_tile = 4 * lpu;
+    launch_seq_lpu<WS, 4, true, 8>(a, lpu, (N + a.ncol_tile - 1) / a.ncol_tile, s);
+  } else if (aligned && N % 2 == 0 && N <= 64) {
+    const int lpu = next_pow2(N / 2);
+    a.ncol_tile = 2 * lpu;
+    launch_seq_lpu<WS, 2, true, 16>(a, lpu, 1, s);
+  } else if (N <= 32) {
     const int lpu = next_pow2(N);
     a.ncol_tile = lpu;
-    switch (lpu) {
-      case 1: launch_seq_t<1, 1, false, 16, WS>(a, 1, s); break;
-      case 2: launch_seq_t<2, 1, false, 16, WS>(a, 1, s); break;
-      case 4: launch_seq_t<4, 1, false, 16, WS>(a, 1, s); break;
-      case 8: launch_seq_t<8, 1, false, 16, WS>(a, 1, s); break;
-      default: launch_seq_t<16, 1, false, 16, WS>(a, 1, s); break;
-    }
+    launch_seq_lpu<WS, 1, false, 16>(a, lpu, 1, s);
+  } else if (N <= 64) {
+    a.ncol_tile = 64;
+    launch_seq_t<32, 2, false, 16, WS>(a, 1, s);
+  } else {
+    a.ncol_tile = 128;
+    launch_seq_t<32, 4, false, 8, WS>(a, (N + 127) / 128, s);
   }
 }
 
@@ -254,7 +292,7 @@ void launch_par_rs_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
   const long long threads = groups_needed * G;
   long long blocks = (threads + 255) / 256;
   blocks = std::max(1LL, std::min(blocks, 148LL * 32));
-  par_rs_kernel<W, VL, CT, V4><<<dim3((unsigned)blocks, ncol_tiles), 256, 0, s>>>(a);
+  par_rs_kernel<W, VL, CT, V4><<<dim3((unsigned)blocks, ncol_tiles), 256, 0, s>>>(a); LAUNCHED(1);
 }
 
 template <int W, int VL>
@@ -289,7 +327,7 @@ template <int W, int CT>
 void launch_par_ws_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
   const int upb = 256 / W;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  par_ws_kernel<W, CT><<<grid, 256, 0, s>>>(a);
+  par_ws_kernel<W, CT><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
 }
 
 template <int W>
@@ -317,9 +355,14 @@ void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   }
 }
 
-// Tiles: ~256 nonzeros per unit (any multiple of the chunk keeps exactness).
-long long tile_chunks(long long chunk) {
-  long long t = 256 / chunk;
+// Tile sizes (nonzeros per work unit).  Any multiple of the chunk keeps the
+// results bit-exact; these are pure performance knobs (env overridable).
+long long env_ll(const char* name, long long dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+long long tile_chunks(long long chunk, long long target) {
+  long long t = target / chunk;
   return t < 1 ? 1 : t;
 }
 
@@ -328,16 +371,17 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   const long long M = h->m;
   if (n == 0 || M == 0) return SPMK_OK;
   if (h->nnz == 0 || h->mne == 0) {
-    zero_all_kernel<<<grid_for(M * n), 256, 0, s>>>(d_y, M * n);
+    zero_all_kernel<<<grid_for(M * n), 256, 0, s>>>(d_y, M * n); LAUNCHED(1);
     CK(cudaGetLastError());
     return SPMK_OK;
   }
   if (n > INT32_MAX / 2) return fail(SPMK_EUNSUPPORTED, "n too large");
+  timing_record(0, s);
   const int N = (int)n;
   const bool aligned = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
   // empty rows -> 0 (the reference's zero-initialised Y)
   if (h->nempty > 0)
-    zero_rows_kernel<<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y);
+    zero_rows_kernel<<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
 
   if (id == SPMK_SEQ_ROWSPLIT || id == SPMK_SEQ_BALANCED) {
     SeqArgs a{};
@@ -352,13 +396,15 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     if (id == SPMK_SEQ_ROWSPLIT) {
       const double avg = (double)h->nnz / (double)h->mne;
-      int rb = (int)std::lround(256.0 / std::max(avg, 1.0));
+      int rb = (int)std::lround((double)env_ll("SPMK_SEQ_TILE_NNZ", 1024) / std::max(avg, 1.0));
       a.RB = std::max(1, std::min(rb, 256));
       a.nunits = (h->mne + a.RB - 1) / a.RB;
+      timing_record(1, s);
       launch_seq<false>(a, aligned, s);
+      timing_record(2, s);
     } else {
       const long long CH = (long long)cfg.seq_chunk;
-      const long long TS = CH * tile_chunks(CH);
+      const long long TS = CH * tile_chunks(CH, env_ll("SPMK_SEQ_TILE_NNZ", 1024));
       Plan& p = get_plan(h, 1, TS, CH, s);
       a.rlo = p.rlo;
       a.TS = TS;
@@ -370,10 +416,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         a.H = sc;
         a.Tsl = sc + (size_t)nch * N;
       }
+      timing_record(1, s);
       launch_seq<true>(a, aligned, s);
+      timing_record(2, s);
       if (p.nlong > 0)
         fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
-            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH);
+            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   } else {
     ParArgs a{};
@@ -388,11 +436,13 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     const int W = (int)cfg.lane_width;
     if (id == SPMK_PAR_ROWSPLIT) {
+      timing_record(1, s);
       launch_par_rs(a, W, aligned, s);
+      timing_record(2, s);
     } else {
       if (W > 32) return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
       const long long CH = W;
-      const long long TS = CH * tile_chunks(CH);
+      const long long TS = CH * kParWsChunksPerTile;  // par_ws_kernel tile shape
       Plan& p = get_plan(h, 2, TS, CH, s);
       a.rlo = p.rlo;
       a.TS = TS;
@@ -403,13 +453,16 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         a.H = sc;
         a.Tsl = sc + (size_t)nch * N;
       }
+      timing_record(1, s);
       launch_par_ws(a, W, aligned, s);
+      timing_record(2, s);
       if (p.nlong > 0)
         fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
-            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH);
+            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   }
   CK(cudaGetLastError());
+  timing_record(3, s);
   return SPMK_OK;
 }
 
@@ -428,7 +481,7 @@ spmk_status create_from_device32(long long m, long long k, long long nnz, int* r
   try {
     int* err = dev_alloc<int>(1);
     CK(cudaMemsetAsync(err, 0, sizeof(int), s));
-    validate_kernel<<<grid_for(std::max(m, 1LL)), 256, 0, s>>>(rp, col, (int)m, (int)k, nnz, err);
+    validate_kernel<<<grid_for(std::max(m, 1LL)), 256, 0, s>>>(rp, col, (int)m, (int)k, nnz, err); LAUNCHED(1);
     CK(cudaGetLastError());
     int herr = 0;
     CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -528,7 +581,7 @@ spmk_status spmk_csr_create(int64_t num_rows, int64_t num_cols, int64_t nnz,
       for (long long o = 0; o < n; o += chunk) {
         const long long c = std::min(chunk, n - o);
         CK(cudaMemcpyAsync(tmp, src + o, c * 8, cudaMemcpyHostToDevice, s));
-        narrow_kernel<<<grid_for(c), 256, 0, s>>>(tmp, dst + o, c, bad);
+        narrow_kernel<<<grid_for(c), 256, 0, s>>>(tmp, dst + o, c, bad); LAUNCHED(1);
         CK(cudaGetLastError());
       }
     };
@@ -626,11 +679,11 @@ spmk_status spmk_csr_slice(spmk_csr_t a, int64_t row_begin, int64_t row_end, int
       CK(cudaMemcpyPeerAsync(tmp, device, a->rp + row_begin, a->device, (rows + 1) * 4, s));
       CK(cudaMemcpyPeerAsync(col, device, a->col + rp_b, a->device, nnz * 4, s));
       CK(cudaMemcpyPeerAsync(val, device, a->val + rp_b, a->device, nnz * 4, s));
-      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(tmp, 0, rows, rp);
+      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(tmp, 0, rows, rp); LAUNCHED(1);
     } else {
       CK(cudaMemcpyAsync(col, a->col + rp_b, nnz * 4, cudaMemcpyDeviceToDevice, s));
       CK(cudaMemcpyAsync(val, a->val + rp_b, nnz * 4, cudaMemcpyDeviceToDevice, s));
-      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(rpsrc, row_begin, rows, rp);
+      rebase_kernel<<<grid_for(rows + 1), 256, 0, s>>>(rpsrc, row_begin, rows, rp); LAUNCHED(1);
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -675,7 +728,7 @@ spmk_status spmk_csr_download(spmk_csr_t a, int64_t* row_ptr, int64_t* col_idx, 
     auto widen = [&](const int* src, int64_t* dst, long long n) {
       if (!dst || n == 0) return;
       long long* tmp = dev_alloc<long long>((size_t)n);
-      widen_kernel<<<grid_for(n), 256>>>(src, tmp, n);
+      widen_kernel<<<grid_for(n), 256>>>(src, tmp, n); LAUNCHED(1);
       CK(cudaGetLastError());
       CK(cudaMemcpy(dst, tmp, n * 8, cudaMemcpyDeviceToHost));
       cudaFree(tmp);
@@ -757,7 +810,7 @@ spmk_status spmk_plan(spmk_csr_t a, int64_t chunk, int64_t* chunk_first_row, int
   DeviceGuard g(a->device);
   try {
     long long* d = dev_alloc<long long>((size_t)nch);
-    chunk_first_row_kernel<<<grid_for(nch), 256>>>(a->rp, (int)a->m, nch, chunk, d);
+    chunk_first_row_kernel<<<grid_for(nch), 256>>>(a->rp, (int)a->m, nch, chunk, d); LAUNCHED(1);
     CK(cudaGetLastError());
     CK(cudaMemcpy(chunk_first_row, d, nch * 8, cudaMemcpyDeviceToHost));
     cudaFree(d);
@@ -773,7 +826,7 @@ spmk_status spmk_plan_elem_row(spmk_csr_t a, int64_t* elem_row) {
   DeviceGuard g(a->device);
   try {
     long long* d = dev_alloc<long long>((size_t)a->nnz);
-    elem_row_kernel<<<grid_for(a->nnz), 256>>>(a->rp, (int)a->m, a->nnz, d);
+    elem_row_kernel<<<grid_for(a->nnz), 256>>>(a->rp, (int)a->m, a->nnz, d); LAUNCHED(1);
     CK(cudaGetLastError());
     CK(cudaMemcpy(elem_row, d, a->nnz * 8, cudaMemcpyDeviceToHost));
     cudaFree(d);
@@ -793,7 +846,7 @@ spmk_status spmk_row_slices(spmk_csr_t a, int64_t parts, int64_t* bounds) {
   DeviceGuard g(a->device);
   try {
     long long* d = dev_alloc<long long>((size_t)parts + 1);
-    row_slices_kernel<<<grid_for(parts + 1), 256>>>(a->rp, (int)a->m, a->nnz, parts, d);
+    row_slices_kernel<<<grid_for(parts + 1), 256>>>(a->rp, (int)a->m, a->nnz, parts, d); LAUNCHED(1);
     CK(cudaGetLastError());
     CK(cudaMemcpy(bounds, d, (parts + 1) * 8, cudaMemcpyDeviceToHost));
     cudaFree(d);
@@ -964,7 +1017,7 @@ spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes) {
 spmk_status spmk_make_dense(int64_t rows, int64_t cols, uint64_t seed, float* d_out, void* stream) {
   const long long total = rows * cols;
   if (total <= 0) return SPMK_OK;
-  make_dense_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(d_out, total, seed);
+  make_dense_kernel<<<grid_for(total), 256, 0, (cudaStream_t)stream>>>(d_out, total, seed); LAUNCHED(1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(SPMK_ECUDA, cudaGetErrorString(e));
   return SPMK_OK;
@@ -994,7 +1047,7 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, d
     unsigned long long* keys = dev_alloc<unsigned long long>((size_t)edges);
     unsigned long long* sorted = dev_alloc<unsigned long long>((size_t)edges);
     rmat_edges_kernel<<<grid_for(edges, 256, 148 * 64), 256, 0, s>>>(keys, edges, (int)scale, seed,
-                                                                     t_a, t_ab, t_abc);
+                                                                     t_a, t_ab, t_abc); LAUNCHED(1);
     CK(cudaGetLastError());
     size_t tb = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, sorted, edges, 0, 2 * (int)scale, s);
@@ -1003,7 +1056,7 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, d
     cudaFree(tmp);
     int* flag = reinterpret_cast<int*>(keys);  // reuse: edges*8 bytes >= 2*edges ints
     int* pos = flag + edges;
-    unique_flag_kernel<<<grid_for(edges), 256, 0, s>>>(sorted, edges, flag);
+    unique_flag_kernel<<<grid_for(edges), 256, 0, s>>>(sorted, edges, flag); LAUNCHED(1);
     size_t sb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, sb, flag, pos, edges, s);
     tmp = dev_alloc<char>(sb);
@@ -1018,11 +1071,11 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, d
     float* val = dev_alloc<float>((size_t)nnz);
     unsigned long long* rows = dev_alloc<unsigned long long>((size_t)nnz);
     unique_scatter_kernel<<<grid_for(edges), 256, 0, s>>>(sorted, edges, flag, pos, (int)scale, col,
-                                                           val, rows);
+                                                           val, rows); LAUNCHED(1);
     cudaFree(keys);
     cudaFree(sorted);
     int* rp = dev_alloc<int>((size_t)m + 1);
-    rowptr_from_rows_kernel<<<grid_for(m + 1), 256, 0, s>>>(rows, nnz, m, rp);
+    rowptr_from_rows_kernel<<<grid_for(m + 1), 256, 0, s>>>(rows, nnz, m, rp); LAUNCHED(1);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
     cudaFree(rows);
@@ -1033,6 +1086,21 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, d
     if (s) cudaStreamDestroy(s);
     return fail(e.st, e.msg);
   }
+}
+
+uint64_t spmk_launch_count(void) { return g_launches.load(); }
+
+spmk_status spmk_timing_enable(int on) {
+  g_timing.on = on != 0;
+  return SPMK_OK;
+}
+
+spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms) {
+  if (!g_timing.on || !g_timing.ev[0]) return fail(SPMK_EINVAL, "timing not enabled / no call recorded");
+  if (cudaEventSynchronize(g_timing.ev[3]) != cudaSuccess) return fail(SPMK_ECUDA, "event sync");
+  if (main_kernel_ms) cudaEventElapsedTime(main_kernel_ms, g_timing.ev[1], g_timing.ev[2]);
+  if (whole_call_ms) cudaEventElapsedTime(whole_call_ms, g_timing.ev[0], g_timing.ev[3]);
+  return SPMK_OK;
 }
 
 }  // extern "C"

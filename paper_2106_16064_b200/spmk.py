@@ -86,6 +86,9 @@ _SIGS = {
     "spmk_kernel_stats": ([vp, C.c_int, P(_Cfg), i64, P(u64), P(u64)], C.c_int),
     "spmk_kernel_tolerance": ([i64], f64),
     "spmk_l2_persist_x": ([vp, vp, C.c_size_t], C.c_int),
+    "spmk_launch_count": ([], u64),
+    "spmk_timing_enable": ([C.c_int], C.c_int),
+    "spmk_timing_last": ([P(f32), P(f32)], C.c_int),
     "spmk_generate_rmat": ([C.c_uint32, u64, f64, f64, f64, f64, u64, C.c_int, P(vp)], C.c_int),
     "spmk_make_dense": ([i64, i64, u64, vp, vp], C.c_int),
 }
@@ -223,7 +226,7 @@ class CsrMatrix:
     def __post_init__(self):
         self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
         self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int64)
-        if np.asarray(self.values).dtype == np.float64:
+        if isinstance(self.values, np.ndarray) and self.values.dtype == np.float64:
             raise UnsupportedError("T=double: the device path is fp32 only")
         self.values = np.ascontiguousarray(self.values, dtype=np.float32)
 
@@ -436,3 +439,19 @@ def l2_persist_x(stream, x, nbytes=None):
     ptr = x.data_ptr() if x is not None else None
     nb = 0 if x is None else (nbytes if nbytes is not None else x.numel() * 4)
     _check(load_library().spmk_l2_persist_x(C.c_void_p(stream.cuda_stream), C.c_void_p(ptr), nb))
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libspmk_b200.so so far (all entry points)."""
+    return int(load_library().spmk_launch_count())
+
+
+def timing_enable(on: bool = True) -> None:
+    _check(load_library().spmk_timing_enable(int(on)))
+
+
+def timing_last():
+    """(dominant-kernel ms, whole-call ms) of the last spmm on this thread."""
+    a, b = f32(), f32()
+    _check(load_library().spmk_timing_last(C.byref(a), C.byref(b)))
+    return a.value, b.value
