@@ -119,6 +119,56 @@ __global__ void tile_plan_kernel(const int* __restrict__ crp, int mne, long long
     rlo[t] = (t == ntiles) ? mne : (int)lower_bound_i32(crp, (long long)mne + 1, t * TS);
   }
 }
+// Per-tile start descriptors (the "K-p" partition plan, computed once per
+// handle and tile shape).  {cur, start, hard_end, mode}:
+//   nonzero-split tiles [t*TS, min((t+1)*TS, nnz)):
+//     cur      compact row containing the first position swept
+//     start    first position swept (> tile start when the entering row is
+//              short and therefore finished by the tile that owns its start)
+//     hard_end last position+1 swept: the tile end, or the end of the row
+//              crossing it when that row ends in the next tile (owner extends)
+//     mode     MODE_ENTER_LONG when the entering row spans >= 2 tile
+//              boundaries (its per-chunk partials go to the H slots), else 0;
+//              start == hard_end marks an empty tile.
+//   row-split tiles (RB compact rows each): {r0, crp[r0], crp[r1], 0}.
+__global__ void ws_tile_desc_kernel(const int* __restrict__ crp, const int* __restrict__ rlo,
+                                    long long ntiles, long long TS, long long nnz,
+                                    int4* __restrict__ desc) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntiles;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long tb = t * TS;
+    const long long te = min(tb + TS, nnz);
+    const int r = rlo[t];
+    long long hard_end = te;
+    if (te < nnz) {
+      const int r2 = rlo[t + 1];
+      const long long c2 = crp[r2];
+      if (c2 > te && crp[r2 - 1] >= tb && c2 <= (t + 2) * TS) hard_end = c2;
+    }
+    int cur = r, mode = MODE_NORMAL;
+    long long start = tb;
+    const long long cr = crp[r];
+    if (cr > tb) {  // row r-1 enters from the left
+      const long long rs = crp[r - 1];
+      if ((cr - 1) / TS - rs / TS >= 2) {
+        cur = r - 1;
+        mode = MODE_ENTER_LONG;
+      } else {
+        start = cr;
+        if (start >= te) hard_end = start;  // nothing to do
+      }
+    }
+    desc[t] = make_int4(cur, (int)start, (int)hard_end, mode);
+  }
+}
+__global__ void rs_tile_desc_kernel(const int* __restrict__ crp, int mne, int RB, long long ntiles,
+                                    int4* __restrict__ desc) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntiles;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r0 = (int)(t * RB), r1 = min(r0 + RB, mne);
+    desc[t] = make_int4(r0, crp[r0], crp[r1], MODE_NORMAL);
+  }
+}
 // Long rows for a tile size: rows spanning >= 2 tile boundaries past their own.
 __global__ void long_rows_kernel(const int* __restrict__ crp, int mne, long long TS,
                                  int* __restrict__ list, int* __restrict__ count) {
@@ -156,13 +206,21 @@ __global__ void row_slices_kernel(const int* __restrict__ rp, int m, long long n
 }
 
 // Zero the empty rows of Y (reference: Y zero-allocated, csr.hpp:66-72).
+// V = 4 when N % 4 == 0 and Y is 16-byte aligned (float4 stores).
+template <int V>
 __global__ void zero_rows_kernel(const int* __restrict__ erow, int ne, int N,
                                  float* __restrict__ Y) {
-  const long long total = (long long)ne * N;
+  const int per_row = N / V;
+  const long long total = (long long)ne * per_row;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const long long r = erow[i / N];
-    __stcs(Y + r * N + (i % N), 0.f);
+    const long long r = erow[i / per_row];
+    float* p = Y + r * N + (i % per_row) * V;
+    if constexpr (V == 4) {
+      __stcs(reinterpret_cast<float4*>(p), make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+      __stcs(p, 0.f);
+    }
   }
 }
 // All of Y zero (nnz == 0 or every row empty).
@@ -174,31 +232,41 @@ __global__ void zero_all_kernel(float* __restrict__ Y, long long total) {
 
 // Long-row fix-up: Y[r] = T[t1] + H[q0] + ... + H[q1] in ascending order
 // (the reference's serial boundary merge, kernels.hpp:316-323 / :448-453,
-// restricted to rows whose partials were not merged in registers).
-__global__ void fixup_kernel(const int* __restrict__ list, int nlong,
-                             const int* __restrict__ crp, const int* __restrict__ rid,
-                             const float* __restrict__ H, const float* __restrict__ Tsl,
-                             float* __restrict__ Y, int N, long long TS, long long CH) {
+// restricted to rows whose partials were not merged in registers).  One block
+// per long row: the row's partials H[q0..q1][0..N) are one contiguous range,
+// staged into shared memory by a coalesced sweep, then each column is summed
+// sequentially (the order is the contract; the adds are the only serial part).
+constexpr int kFixupSmemFloats = 12288;  // 48 KB
+__global__ void __launch_bounds__(256)
+fixup_kernel(const int* __restrict__ list, int nlong,
+             const int* __restrict__ crp, const int* __restrict__ rid,
+             const float* __restrict__ H, const float* __restrict__ Tsl,
+             float* __restrict__ Y, int N, long long TS, long long CH) {
+  __shared__ float sm[kFixupSmemFloats];
   const long long T = TS / CH;
-  const long long total = (long long)nlong * N;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c = list[i / N];
-    const int j = (int)(i % N);
+  for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
+    const int c = list[li];
     const long long s = crp[c], f = crp[c + 1];
     const long long t1 = s / TS;
     const long long q0 = (t1 + 1) * T, q1 = (f - 1) / CH;
-    float acc = Tsl[t1 * N + j];
-    long long q = q0;
-    for (; q + 8 <= q1 + 1; q += 8) {
-      float h[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) h[u] = H[(q + u) * N + j];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, h[u]);
+    const float* Yrow_dummy = nullptr;
+    (void)Yrow_dummy;
+    for (int j0 = 0; j0 < N; j0 += 256) {  // column block handled by threads j < 256
+      const int j = j0 + threadIdx.x;
+      float acc = (j < N) ? Tsl[t1 * N + j] : 0.f;
+      const long long qpb = max(1LL, (long long)kFixupSmemFloats / N);  // partials per smem batch
+      for (long long qb = q0; qb <= q1; qb += qpb) {
+        const long long qe = min(q1 + 1, qb + qpb);
+        const long long cnt = (qe - qb) * N;
+        __syncthreads();
+        for (long long i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = H[qb * N + i];
+        __syncthreads();
+        if (j < N) {
+          for (long long q = 0; q < qe - qb; ++q) acc = __fadd_rn(acc, sm[q * N + j]);
+        }
+      }
+      if (j < N) Y[(long long)rid[c] * N + j] = acc;
     }
-    for (; q <= q1; ++q) acc = __fadd_rn(acc, H[q * N + j]);
-    Y[(long long)rid[c] * N + j] = acc;
   }
 }
 

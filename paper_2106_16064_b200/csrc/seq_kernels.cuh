@@ -46,6 +46,7 @@ struct SeqArgs {
   float* __restrict__ Tsl;       // tile prefix slots (ntiles x N)
   const int* __restrict__ rlo;   // ws: first compact row starting >= tile start
   const int* __restrict__ order; // rs: tile processing order (heavy first) or null
+  const int4* __restrict__ desc; // per-tile start descriptors (ws_/rs_tile_desc_kernel)
   int mne;                       // non-empty rows
   int nnz;
   int N;                         // columns of X / Y
@@ -63,80 +64,23 @@ struct SeqWin {
   static constexpr int WIN = LPU >= 8 ? 64 : (LPU >= 2 ? 32 : 16);
 };
 
-template <int LPU, int CPL, bool VEC, int B, bool WS>
-__global__ void __launch_bounds__(kSeqThreads, 2)
-seq_kernel(const SeqArgs a) {
-  constexpr int SLOTS = (B + LPU - 1) / LPU;  // entries loaded per lane per batch
-  constexpr int WIN = SeqWin<LPU>::WIN;
-  constexpr int NGROUPS = kSeqThreads / LPU;
-  constexpr int BIG = 0x7fffffff;
-  __shared__ int s_win[NGROUPS * 2 * WIN];
+// Per-group sweep state: tile setup, the row window and the (rare) event
+// handler.  Every member function is force-inlined, so the state lives in
+// registers; the two kernels below differ only in how dense rows arrive.
+template <int LPU, int CPL, bool VEC, bool WS>
+struct SeqSweep {
+  static constexpr int WIN = SeqWin<LPU>::WIN;
+  static constexpr int BIG = 0x7fffffff;
+  int e, te, hard_end, cur, cur_end, orow, mode, q, next_cb, long_thresh, CH, wb, unit, nev;
+  bool live;
+  float carry[CPL], acc[CPL];
+  int* wcrp;  // wcrp[i] = crp[wb + 1 + i]
+  int* wrid;  // wrid[i] = rid[wb + i]
+  int gl, col0, N;
+  unsigned gmask;
+  ColMap<LPU, CPL, VEC> cm;
 
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (LPU - 1);
-  const int gidx = threadIdx.x / LPU;
-  const unsigned gmask = group_mask<LPU>();
-  int unit = blockIdx.x * NGROUPS + gidx;
-  // Every lane of the warp stays in the sweep loop until all groups are done
-  // (warp-uniform trip count), so all shuffles run converged on a full mask.
-  bool live = unit < a.nunits;
-  if (!live) unit = 0;
-  if constexpr (!WS) {
-    if (a.order && live) unit = a.order[unit];
-  }
-  int* wcrp = s_win + gidx * 2 * WIN;  // wcrp[i] = crp[wb + 1 + i]
-  int* wrid = wcrp + WIN;              // wrid[i] = rid[wb + i]
-
-  const int col0 = blockIdx.y * a.ncol_tile;
-  const ColMap<LPU, CPL, VEC> cm{gl, min(a.ncol_tile, a.N - col0)};
-  const int N = a.N;
-  const uint64_t pol = evict_first_policy();
-
-  // ---- tile setup (all divisions happen here, none in the sweep) ----------
-  int e, te, hard_end, cur;
-  int mode = MODE_NORMAL;
-  int q = 0, next_cb = BIG, long_thresh = BIG, CH = BIG;
-  if constexpr (WS) {
-    CH = (int)a.CH;
-    const long long tb = (long long)unit * a.TS;
-    te = (int)min(tb + a.TS, (long long)a.nnz);
-    long_thresh = (int)min((long long)(unit + 2) * a.TS, (long long)BIG);  // row end > this => long
-    const int r = a.rlo[unit];
-    hard_end = te;
-    if (te < a.nnz) {  // row crossing te, finished here if it ends in the next tile
-      const int r2 = a.rlo[unit + 1];
-      const int c2 = a.crp[r2];
-      if (c2 > te && a.crp[r2 - 1] >= tb && c2 <= long_thresh) hard_end = c2;
-    }
-    const int cr = a.crp[r];
-    if (cr > tb) {  // row r-1 enters from the left
-      const int rs = a.crp[r - 1];
-      if ((cr - 1) / a.TS - rs / a.TS >= 2) {
-        cur = r - 1;
-        mode = MODE_ENTER_LONG;
-        e = (int)tb;
-      } else {
-        e = cr;  // skipped: finished by its owner tile
-        if (e >= te) live = false;
-        cur = r;
-      }
-    } else {
-      e = (int)tb;
-      cur = r;
-    }
-    q = e / CH;
-    next_cb = (int)min((long long)(q + 1) * CH, (long long)BIG);
-  } else {
-    const int r0 = unit * a.RB;
-    const int r1 = min(r0 + a.RB, a.mne);
-    e = a.crp[r0];
-    te = a.crp[r1];
-    hard_end = te;
-    cur = r0;
-  }
-
-  int wb = cur;
-  auto refill = [&](int base) {
+  __device__ __forceinline__ void refill(const SeqArgs& a, int base) {
     __syncwarp(gmask);
 #pragma unroll 1
     for (int i = gl; i < WIN; i += LPU) {
@@ -146,23 +90,131 @@ seq_kernel(const SeqArgs a) {
     }
     __syncwarp(gmask);
     wb = base;
-  };
-  refill(cur);
-  int cur_end = wcrp[0];
-  int orow = wrid[0];
-  if (WS && mode == MODE_NORMAL && cur_end > long_thresh) mode = MODE_OWNER_LONG;
-  float carry[CPL], acc[CPL];
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) carry[k] = acc[k] = 0.f;
-  int nev = min(cur_end, next_cb);
+  }
 
-  // ---- pipelined sweep -----------------------------------------------------
+  // Tile setup, part 1: one 16-byte descriptor load (the plan precomputed the
+  // entering/crossing-row decisions), so the colIdx/val prefetch can be issued
+  // right after it without further dependent round trips.
+  __device__ __forceinline__ void setup_begin(const SeqArgs& a, int* swin) {
+    const int lane = threadIdx.x & 31;
+    gl = lane & (LPU - 1);
+    const int gidx = threadIdx.x / LPU;
+    gmask = group_mask<LPU>();
+    constexpr int NGROUPS = kSeqThreads / LPU;
+    unit = blockIdx.x * NGROUPS + gidx;
+    // Every lane of the warp stays in the sweep loop until all groups are done
+    // (warp-uniform trip count), so all shuffles run converged on a full mask.
+    live = unit < a.nunits;
+    if (!live) unit = 0;
+    if constexpr (!WS) {
+      if (a.order && live) unit = a.order[unit];
+    }
+    wcrp = swin + gidx * 2 * WIN;
+    wrid = wcrp + WIN;
+    col0 = blockIdx.y * a.ncol_tile;
+    cm = ColMap<LPU, CPL, VEC>{gl, min(a.ncol_tile, a.N - col0)};
+    N = a.N;
+    const int4 d = a.desc[unit];
+    cur = d.x;
+    e = d.y;
+    hard_end = d.z;
+    mode = d.w;
+    q = 0;
+    next_cb = BIG;
+    long_thresh = BIG;
+    CH = BIG;
+    if constexpr (WS) {
+      CH = (int)a.CH;
+      const long long tb = (long long)unit * a.TS;
+      te = (int)min(tb + a.TS, (long long)a.nnz);
+      long_thresh = (int)min((long long)(unit + 2) * a.TS, (long long)BIG);  // row end > this => long
+      q = e / CH;
+      next_cb = (int)min((long long)(q + 1) * CH, (long long)BIG);
+    } else {
+      te = hard_end;
+    }
+    if (e >= hard_end) live = false;
+    if (!live) hard_end = 0;  // no loads for idle groups
+  }
+  // Tile setup, part 2 (after the prefetch is in flight): the row window.
+  __device__ __forceinline__ void setup_end(const SeqArgs& a) {
+    refill(a, cur);
+    cur_end = wcrp[0];
+    orow = wrid[0];
+    if (WS && mode == MODE_NORMAL && cur_end > long_thresh) mode = MODE_OWNER_LONG;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) carry[k] = acc[k] = 0.f;
+    nev = min(cur_end, next_cb);
+  }
+
+  // Events at position p (before consuming it): row end and/or chunk boundary.
+  __device__ __forceinline__ void event(const SeqArgs& a, int p) {
+    if (p == cur_end) {
+      if (WS && mode == MODE_ENTER_LONG) {
+        cm.store_slot(a.H + (size_t)q * N + col0, acc);
+      } else {
+        float o[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) o[k] = __fadd_rn(carry[k], acc[k]);
+        cm.store(a.Y + (size_t)orow * N + col0, o);
+      }
+      if (p >= te) {
+        live = false;
+      } else {
+        ++cur;
+        if (cur - wb >= WIN) refill(a, cur);
+        cur_end = wcrp[cur - wb];
+        orow = wrid[cur - wb];
+        mode = (WS && cur_end > long_thresh) ? MODE_OWNER_LONG : MODE_NORMAL;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) carry[k] = acc[k] = 0.f;
+      }
+    }
+    if (WS && live && p == next_cb) {
+      if (mode == MODE_ENTER_LONG) {
+        cm.store_slot(a.H + (size_t)q * N + col0, acc);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[k] = 0.f;
+        if (p >= te) live = false;
+      } else if (mode == MODE_OWNER_LONG && p >= te) {
+        float o[CPL];
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) o[k] = __fadd_rn(carry[k], acc[k]);
+        cm.store_slot(a.Tsl + (size_t)unit * N + col0, o);
+        live = false;
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          carry[k] = __fadd_rn(carry[k], acc[k]);
+          acc[k] = 0.f;
+        }
+      }
+      ++q;
+      next_cb = (next_cb > BIG - CH) ? BIG : next_cb + CH;
+    }
+    nev = min(cur_end, next_cb);
+  }
+};
+
+// --------------------------------------------------------------------------
+// Register-pipelined sweep (any column mapping).
+// --------------------------------------------------------------------------
+template <int LPU, int CPL, bool VEC, int B, bool WS>
+__global__ void __launch_bounds__(kSeqThreads, 2)
+seq_kernel(const SeqArgs a) {
+  constexpr int SLOTS = (B + LPU - 1) / LPU;  // entries loaded per lane per batch
+  using SW = SeqSweep<LPU, CPL, VEC, WS>;
+  __shared__ int s_win[(kSeqThreads / LPU) * 2 * SW::WIN];
+  SW st;
+  st.setup_begin(a, s_win);
+  const uint64_t pol = evict_first_policy();
+
   auto load_cv = [&](int eb, int (&cr)[SLOTS], float (&vr)[SLOTS]) {
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
-      const int o = s * LPU + gl;
+      const int o = s * LPU + st.gl;
       const int p = eb + o;
-      if (o < B && p < hard_end) {
+      if (o < B && p < st.hard_end) {
         if constexpr (LPU >= 8) {
           cr[s] = ld_stream(a.col + p, pol);
           vr[s] = ld_stream(a.val + p, pol);
@@ -180,8 +232,8 @@ seq_kernel(const SeqArgs a) {
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const int c = gshfl<LPU>(cr[j / LPU], j % LPU);
-      if (eb + j < hard_end) {
-        cm.load(a.X + (size_t)c * N + col0, xv[j]);
+      if (eb + j < st.hard_end) {
+        st.cm.load(a.X + (size_t)c * st.N + st.col0, xv[j]);
       } else {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) xv[j][k] = 0.f;
@@ -192,13 +244,13 @@ seq_kernel(const SeqArgs a) {
   int c_c[SLOTS], c_n[SLOTS], c_nn[SLOTS];
   float v_c[SLOTS], v_n[SLOTS], v_nn[SLOTS];
   float x_c[B][CPL], x_n[B][CPL];
-  load_cv(e, c_c, v_c);
-  load_cv(e + B, c_n, v_n);
-  load_x(e, c_c, x_c);
+  load_cv(st.e, c_c, v_c);
+  load_cv(st.e + B, c_n, v_n);
+  st.setup_end(a);
+  load_x(st.e, c_c, x_c);
 
-  if (!live) hard_end = 0;  // no loads for idle groups
 #pragma unroll 1
-  for (int eb = e; __any_sync(0xffffffffu, live); eb += B) {
+  for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += B) {
     load_cv(eb + 2 * B, c_nn, v_nn);
     load_x(eb + B, c_n, x_n);
     float vv[B];
@@ -210,61 +262,17 @@ seq_kernel(const SeqArgs a) {
     // groups may diverge here.
     int js = 0;
 #pragma unroll 1
-    while (live) {
-      const int je = (nev < eb + B) ? nev - eb : B;
+    while (st.live) {
+      const int je = (st.nev < eb + B) ? st.nev - eb : B;
 #pragma unroll
       for (int j = 0; j < B; ++j) {
         if (j >= js && j < je) {
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) acc[k] = mul_add_rn(acc[k], vv[j], x_c[j][k]);
+          for (int k = 0; k < CPL; ++k) st.acc[k] = mul_add_rn(st.acc[k], vv[j], x_c[j][k]);
         }
       }
       if (je >= B) break;
-      const int p = eb + je;  // event before consuming position p
-      if (p == cur_end) {
-        if (WS && mode == MODE_ENTER_LONG) {
-          cm.store_slot(a.H + (size_t)q * N + col0, acc);
-        } else {
-          float o[CPL];
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) o[k] = __fadd_rn(carry[k], acc[k]);
-          cm.store(a.Y + (size_t)orow * N + col0, o);
-        }
-        if (p >= te) {
-          live = false;
-        } else {
-          ++cur;
-          if (cur - wb >= WIN) refill(cur);
-          cur_end = wcrp[cur - wb];
-          orow = wrid[cur - wb];
-          mode = (WS && cur_end > long_thresh) ? MODE_OWNER_LONG : MODE_NORMAL;
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) carry[k] = acc[k] = 0.f;
-        }
-      }
-      if (WS && live && p == next_cb) {
-        if (mode == MODE_ENTER_LONG) {
-          cm.store_slot(a.H + (size_t)q * N + col0, acc);
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) acc[k] = 0.f;
-          if (p >= te) live = false;
-        } else if (mode == MODE_OWNER_LONG && p >= te) {
-          float o[CPL];
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) o[k] = __fadd_rn(carry[k], acc[k]);
-          cm.store_slot(a.Tsl + (size_t)unit * N + col0, o);
-          live = false;
-        } else {
-#pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            carry[k] = __fadd_rn(carry[k], acc[k]);
-            acc[k] = 0.f;
-          }
-        }
-        ++q;
-        next_cb = (next_cb > BIG - CH) ? BIG : next_cb + CH;
-      }
-      nev = min(cur_end, next_cb);
+      st.event(a, eb + je);
       js = je;
     }
     // rotate the pipeline
@@ -279,6 +287,132 @@ seq_kernel(const SeqArgs a) {
       v_n[s] = v_nn[s];
     }
   }
+}
+
+// --------------------------------------------------------------------------
+// Shared-memory-staged sweep for 4-aligned widths (float4 per lane): the
+// dense-row gathers are cp.async (LDGSTS) 16-byte copies into an S-stage ring,
+// so the bytes in flight live in shared memory, not registers.  Each lane
+// reads back exactly the 16 bytes it copied, so completion is the per-thread
+// cp.async.wait_group — no cross-lane barrier.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(unsigned smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(NPEND));
+}
+
+template <int LPU, int B, int S>
+constexpr int seq_async_smem_bytes() {
+  return 256 * S * B * 16 + (256 / LPU) * 2 * SeqWin<LPU>::WIN * 4;
+}
+
+template <int LPU, int B, int S, bool WS>
+__global__ void __launch_bounds__(kSeqThreads, 2)
+seq_kernel_async(const SeqArgs a) {
+  constexpr int SLOTS = (B + LPU - 1) / LPU;
+  using SW = SeqSweep<LPU, 4, true, WS>;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  float4* ring = reinterpret_cast<float4*>(s_dyn);  // [S][B][256 threads]
+  int* s_win = reinterpret_cast<int*>(s_dyn + 256 * S * B * 16);
+  SW st;
+  st.setup_begin(a, s_win);
+  const uint64_t pol = evict_first_policy();
+  const bool colok = 4 * st.gl < st.cm.nt;
+  const unsigned ring_base = (unsigned)__cvta_generic_to_shared(ring) + threadIdx.x * 16;
+  const float* xg = a.X + st.col0 + 4 * st.gl;
+
+  auto load_cv = [&](int eb, int (&cr)[SLOTS], float (&vr)[SLOTS]) {
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int o = s * LPU + st.gl;
+      const int p = eb + o;
+      if (o < B && p < st.hard_end) {
+        if constexpr (LPU >= 8) {
+          cr[s] = ld_stream(a.col + p, pol);
+          vr[s] = ld_stream(a.val + p, pol);
+        } else {
+          cr[s] = __ldg(a.col + p);
+          vr[s] = __ldg(a.val + p);
+        }
+      } else {
+        cr[s] = 0;
+        vr[s] = 0.f;
+      }
+    }
+  };
+  // issue the gathers of batch `eb` into ring stage `stg`
+  auto issue = [&](int eb, int stg, const int (&cr)[SLOTS]) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const int c = gshfl<LPU>(cr[j / LPU], j % LPU);
+      if (colok && eb + j < st.hard_end)
+        cp_async16(ring_base + (unsigned)((stg * B + j) * 256 * 16), xg + (size_t)c * st.N);
+    }
+    cp_async_commit();
+  };
+
+  // Pipeline depths: colIdx/val are loaded R-1 batches ahead of consumption
+  // (they stream from HBM), dense rows are gathered S-1 batches ahead.
+  constexpr int R = S + 4;
+  int cring[R][SLOTS];
+  float vring[R][SLOTS];
+#pragma unroll
+  for (int r = 0; r < R - 1; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
+  st.setup_end(a);
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) issue(st.e + s * B, s, cring[s]);
+
+  int stage = 0;
+#pragma unroll 1
+  for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += B) {
+    load_cv(eb + (R - 1) * B, cring[R - 1], vring[R - 1]);
+    issue(eb + (S - 1) * B, (stage + S - 1) % S, cring[S - 1]);
+    cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
+    // products of the whole batch up front (smem latency off the add chain);
+    // positions that end up unconsumed are simply never added
+    const float4* xs = ring + stage * B * 256 + threadIdx.x;
+    float pr[B][4];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const float v = gshfl<LPU>(vring[0][j / LPU], j % LPU);
+      const float4 x = xs[j * 256];
+      pr[j][0] = __fmul_rn(v, x.x);
+      pr[j][1] = __fmul_rn(v, x.y);
+      pr[j][2] = __fmul_rn(v, x.z);
+      pr[j][3] = __fmul_rn(v, x.w);
+    }
+    // Consume in rounds: every group adds its products up to its next event
+    // (predicated adds, no branches), then all groups that reached an event
+    // handle it together (converged), until the batch is done.
+    int js = st.live ? 0 : B;
+#pragma unroll 1
+    while (true) {
+      const int je = st.live ? min(B, st.nev - eb) : B;
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const bool m = j >= js && j < je;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st.acc[k] = m ? __fadd_rn(st.acc[k], pr[j][k]) : st.acc[k];
+      }
+      const bool ev = st.live && je < B;
+      if (!__any_sync(0xffffffffu, ev)) break;
+      if (ev) st.event(a, eb + je);
+      js = ev ? je : B;
+    }
+    stage = (stage + 1 == S) ? 0 : stage + 1;
+#pragma unroll
+    for (int r = 0; r + 1 < R; ++r)
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        cring[r][s] = cring[r + 1][s];
+        vring[r][s] = vring[r + 1][s];
+      }
+  }
+  cp_async_wait<0>();
 }
 
 }  // namespace spmk_dev

@@ -61,6 +61,7 @@ T* dev_alloc(size_t count) {
 }
 
 struct Plan {
+  int4* desc = nullptr;    // ntiles per-tile start descriptors
   int* rlo = nullptr;      // ntiles + 1
   long long ntiles = 0;
   long long TS = 0, CH = 0;
@@ -141,6 +142,7 @@ void free_handle(spmk_csr_s* h) {
   cudaFree(h->erow);
   for (auto& kv : h->plans) {
     cudaFree(kv.second.rlo);
+    cudaFree(kv.second.desc);
     cudaFree(kv.second.longrows);
   }
   cudaFree(h->scratch);
@@ -198,6 +200,8 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t
   p.ntiles = (h->nnz + TS - 1) / TS;
   p.rlo = dev_alloc<int>((size_t)p.ntiles + 1);
   tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo); LAUNCHED(1);
+  p.desc = dev_alloc<int4>((size_t)p.ntiles);
+  ws_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, p.rlo, p.ntiles, TS, h->nnz, p.desc); LAUNCHED(1);
   int* cnt = dev_alloc<int>(1);
   CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
   // upper bound on long rows: nnz / (TS+1)
@@ -210,6 +214,19 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t
   CK(cudaStreamSynchronize(s));
   cudaFree(cnt);
   return h->plans.emplace(key, p).first->second;
+}
+
+// Row-split tile descriptors (RB compact rows per tile), cached like a plan.
+int4* get_rs_desc(spmk_csr_s* h, int RB, cudaStream_t s) {
+  auto key = std::make_tuple(3, (long long)RB, 0LL);
+  auto it = h->plans.find(key);
+  if (it != h->plans.end()) return it->second.desc;
+  Plan p;
+  p.ntiles = (h->mne + RB - 1) / RB;
+  p.desc = dev_alloc<int4>((size_t)p.ntiles);
+  rs_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, h->mne, RB, p.ntiles, p.desc); LAUNCHED(1);
+  CK(cudaGetLastError());
+  return h->plans.emplace(key, p).first->second.desc;
 }
 
 float* get_scratch(spmk_csr_s* h, size_t floats) {
@@ -237,6 +254,11 @@ int next_pow2(int x) {
   return p;
 }
 
+long long env_ll(const char* name, long long dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+
 // ------------------------------------------------------------ seq launch
 template <int LPU, int CPL, bool VEC, int B, bool WS>
 void launch_seq_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
@@ -260,13 +282,42 @@ void launch_seq_lpu(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   }
 }
 
+template <int LPU, int B, int S, bool WS>
+void launch_seq_async_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
+  constexpr int smem = seq_async_smem_bytes<LPU, B, S>();
+  static bool attr_set = false;  // per instantiation (host-side, benign race)
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(seq_kernel_async<LPU, B, S, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const int upb = 256 / LPU;
+  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
+  seq_kernel_async<LPU, B, S, WS><<<grid, 256, smem, s>>>(a);
+}
+
+template <bool WS, int B, int S>
+void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+  switch (lpu) {
+    case 1: launch_seq_async_t<1, B, S, WS>(a, tiles, s); break;
+    case 2: launch_seq_async_t<2, B, S, WS>(a, tiles, s); break;
+    case 4: launch_seq_async_t<4, B, S, WS>(a, tiles, s); break;
+    case 8: launch_seq_async_t<8, B, S, WS>(a, tiles, s); break;
+    case 16: launch_seq_async_t<16, B, S, WS>(a, tiles, s); break;
+    default: launch_seq_async_t<32, B, S, WS>(a, tiles, s); break;
+  }
+}
+
 template <bool WS>
 void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
   const int N = a.N;
   if (aligned && N % 4 == 0) {
     const int lpu = std::min(32, next_pow2(N / 4));
     a.ncol_tile = 4 * lpu;
-    launch_seq_lpu<WS, 4, true, 8>(a, lpu, (N + a.ncol_tile - 1) / a.ncol_tile, s);
+    const int tiles = (N + a.ncol_tile - 1) / a.ncol_tile;
+    const long long variant = env_ll("SPMK_SEQ_VARIANT", 1);
+    if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
+    else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
+    else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
     const int lpu = next_pow2(N / 2);
     a.ncol_tile = 2 * lpu;
@@ -357,10 +408,6 @@ void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
 
 // Tile sizes (nonzeros per work unit).  Any multiple of the chunk keeps the
 // results bit-exact; these are pure performance knobs (env overridable).
-long long env_ll(const char* name, long long dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoll(v) : dflt;
-}
 long long tile_chunks(long long chunk, long long target) {
   long long t = target / chunk;
   return t < 1 ? 1 : t;
@@ -380,8 +427,13 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   const int N = (int)n;
   const bool aligned = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
   // empty rows -> 0 (the reference's zero-initialised Y)
-  if (h->nempty > 0)
-    zero_rows_kernel<<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+  if (h->nempty > 0) {
+    if (aligned && N % 4 == 0) {
+      zero_rows_kernel<4><<<grid_for((long long)h->nempty * N / 4), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+    } else {
+      zero_rows_kernel<1><<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+    }
+  }
 
   if (id == SPMK_SEQ_ROWSPLIT || id == SPMK_SEQ_BALANCED) {
     SeqArgs a{};
@@ -396,17 +448,19 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     if (id == SPMK_SEQ_ROWSPLIT) {
       const double avg = (double)h->nnz / (double)h->mne;
-      int rb = (int)std::lround((double)env_ll("SPMK_SEQ_TILE_NNZ", 1024) / std::max(avg, 1.0));
+      int rb = (int)std::lround((double)env_ll("SPMK_SEQ_TILE_NNZ", 256) / std::max(avg, 1.0));
       a.RB = std::max(1, std::min(rb, 256));
       a.nunits = (h->mne + a.RB - 1) / a.RB;
+      a.desc = get_rs_desc(h, a.RB, s);
       timing_record(1, s);
       launch_seq<false>(a, aligned, s);
       timing_record(2, s);
     } else {
       const long long CH = (long long)cfg.seq_chunk;
-      const long long TS = CH * tile_chunks(CH, env_ll("SPMK_SEQ_TILE_NNZ", 1024));
+      const long long TS = CH * tile_chunks(CH, env_ll("SPMK_SEQ_TILE_NNZ", 256));
       Plan& p = get_plan(h, 1, TS, CH, s);
       a.rlo = p.rlo;
+      a.desc = p.desc;
       a.TS = TS;
       a.CH = CH;
       a.nunits = (int)p.ntiles;
@@ -420,7 +474,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_seq<true>(a, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
+        fixup_kernel<<<std::min(p.nlong, 148 * 8), 256, 0, s>>>(
             p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   } else {
@@ -457,7 +511,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws(a, W, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<grid_for((long long)p.nlong * N), 256, 0, s>>>(
+        fixup_kernel<<<std::min(p.nlong, 148 * 8), 256, 0, s>>>(
             p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   }
