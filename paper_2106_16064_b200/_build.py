@@ -67,7 +67,7 @@ def build_cpp_tests(verbose: bool = True) -> str:
                          for f in os.listdir(os.path.join(ROOT, "include", "spmk"))]
     if _stale(out, deps):
         cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-o", out, src,
-               "-L", PKG, "-lspmk_b200", f"-Wl,-rpath,{PKG}", "-pthread"]
+               "-L", PKG, "-lspmk_b200", "-Wl,-rpath,$ORIGIN/../../paper_2106_16064_b200", "-pthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
