@@ -249,8 +249,6 @@ fixup_kernel(const int* __restrict__ list, int nlong,
     const long long s = crp[c], f = crp[c + 1];
     const long long t1 = s / TS;
     const long long q0 = (t1 + 1) * T, q1 = (f - 1) / CH;
-    const float* Yrow_dummy = nullptr;
-    (void)Yrow_dummy;
     for (int j0 = 0; j0 < N; j0 += 256) {  // column block handled by threads j < 256
       const int j = j0 + threadIdx.x;
       float acc = (j < N) ? Tsl[t1 * N + j] : 0.f;

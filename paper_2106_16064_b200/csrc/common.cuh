@@ -40,6 +40,18 @@ __device__ __forceinline__ float ld_stream(const float* ptr, uint64_t pol) {
                : "=f"(v) : "l"(ptr), "l"(pol));
   return v;
 }
+__device__ __forceinline__ int4 ld_stream4(const int* ptr, uint64_t pol) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_stream4(const float* ptr, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+  return v;
+}
 // X gathers: read-only path, normal L1 allocation (hub columns repeat).
 __device__ __forceinline__ float ld_x(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float2 ld_x2(const float* p) {

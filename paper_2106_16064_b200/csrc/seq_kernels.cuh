@@ -55,6 +55,7 @@ struct SeqArgs {
   long long CH;                  // ws: chunk size (seq_chunk)
   int RB;                        // rs: rows per tile
   int nunits;                    // tiles
+  int cvvec;                     // colIdx/val 16-byte aligned (vector batch loads)
 };
 
 constexpr int kSeqThreads = 256;
@@ -67,7 +68,7 @@ struct SeqWin {
 // Per-group sweep state: tile setup, the row window and the (rare) event
 // handler.  Every member function is force-inlined, so the state lives in
 // registers; the two kernels below differ only in how dense rows arrive.
-template <int LPU, int CPL, bool VEC, bool WS>
+template <int LPU, int CPL, bool VEC, bool WS, int NT = kSeqThreads>
 struct SeqSweep {
   static constexpr int WIN = SeqWin<LPU>::WIN;
   static constexpr int BIG = 0x7fffffff;
@@ -100,7 +101,7 @@ struct SeqSweep {
     gl = lane & (LPU - 1);
     const int gidx = threadIdx.x / LPU;
     gmask = group_mask<LPU>();
-    constexpr int NGROUPS = kSeqThreads / LPU;
+    constexpr int NGROUPS = NT / LPU;
     unit = blockIdx.x * NGROUPS + gidx;
     // Every lane of the warp stays in the sweep loop until all groups are done
     // (warp-uniform trip count), so all shuffles run converged on a full mask.
@@ -299,25 +300,28 @@ seq_kernel(const SeqArgs a) {
 __device__ __forceinline__ void cp_async16(unsigned smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
 }
+__device__ __forceinline__ void cp_async16_ca(unsigned smem, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(NPEND));
 }
 
-template <int LPU, int B, int S>
+template <int LPU, int B, int S, int NT>
 constexpr int seq_async_smem_bytes() {
-  return 256 * S * B * 16 + (256 / LPU) * 2 * SeqWin<LPU>::WIN * 4;
+  return NT * S * B * 16 + (NT / LPU) * 2 * SeqWin<LPU>::WIN * 4;
 }
 
-template <int LPU, int B, int S, bool WS>
-__global__ void __launch_bounds__(kSeqThreads, 2)
+template <int LPU, int B, int S, bool WS, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
 seq_kernel_async(const SeqArgs a) {
   constexpr int SLOTS = (B + LPU - 1) / LPU;
-  using SW = SeqSweep<LPU, 4, true, WS>;
+  using SW = SeqSweep<LPU, 4, true, WS, NT>;
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  float4* ring = reinterpret_cast<float4*>(s_dyn);  // [S][B][256 threads]
-  int* s_win = reinterpret_cast<int*>(s_dyn + 256 * S * B * 16);
+  float4* ring = reinterpret_cast<float4*>(s_dyn);  // [S][B][NT threads]
+  int* s_win = reinterpret_cast<int*>(s_dyn + NT * S * B * 16);
   SW st;
   st.setup_begin(a, s_win);
   const uint64_t pol = evict_first_policy();
@@ -350,7 +354,7 @@ seq_kernel_async(const SeqArgs a) {
     for (int j = 0; j < B; ++j) {
       const int c = gshfl<LPU>(cr[j / LPU], j % LPU);
       if (colok && eb + j < st.hard_end)
-        cp_async16(ring_base + (unsigned)((stg * B + j) * 256 * 16), xg + (size_t)c * st.N);
+        cp_async16(ring_base + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)c * st.N);
     }
     cp_async_commit();
   };
@@ -374,12 +378,12 @@ seq_kernel_async(const SeqArgs a) {
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     // products of the whole batch up front (smem latency off the add chain);
     // positions that end up unconsumed are simply never added
-    const float4* xs = ring + stage * B * 256 + threadIdx.x;
+    const float4* xs = ring + stage * B * NT + threadIdx.x;
     float pr[B][4];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const float v = gshfl<LPU>(vring[0][j / LPU], j % LPU);
-      const float4 x = xs[j * 256];
+      const float4 x = xs[j * NT];
       pr[j][0] = __fmul_rn(v, x.x);
       pr[j][1] = __fmul_rn(v, x.y);
       pr[j][2] = __fmul_rn(v, x.z);
@@ -410,6 +414,264 @@ seq_kernel_async(const SeqArgs a) {
       for (int s = 0; s < SLOTS; ++s) {
         cring[r][s] = cring[r + 1][s];
         vring[r][s] = vring[r + 1][s];
+      }
+  }
+  cp_async_wait<0>();
+}
+
+}  // namespace spmk_dev
+
+namespace spmk_dev {
+
+// --------------------------------------------------------------------------
+// Register-pipelined sweep for 4-aligned widths (every lane owns a float4 of
+// the column tile; LPU = column tile / 4 lanes per unit), the production
+// seq-rs / seq-ws kernel for N % 4 == 0.
+//   * colIdx/val of a batch of B nonzeros are loaded by every lane of the unit
+//     as 16-byte broadcast vectors (CSC: the sparse tile is
+//     read coalesced once per unit and shared by all its lanes), two batches
+//     ahead of consumption; dense-row float4 gathers one batch ahead, into
+//     registers through the L1-allocating read-only path, so hot dense rows
+//     of power-law matrices hit in L1.
+//   * loads are never predicated per element: the sweep runs over B-aligned
+//     batches; positions outside [e, hard_end) read harmless in-bounds data
+//     and are excluded from the sums (value 0 before e while acc is +0; the
+//     unit stops at its final event at hard_end).
+//   * events (row end / chunk boundary) are located per batch with one
+//     REDUX.OR over the units' next-event bits; the unrolled consume loop
+//     branches (warp-uniformly) only at positions where some unit has one.
+// EXACT: acc = acc + rn(v*x) (the reference's two roundings, bit-identical);
+// otherwise one FFMA per column (fast mode, within the stated tolerance).
+// --------------------------------------------------------------------------
+template <int LPU, int B, bool WS, bool EXACT>
+__global__ void __launch_bounds__(kSeqThreads, 2)
+seq4_kernel(const SeqArgs a) {
+  static_assert(B % 4 == 0 && B <= 16, "B");
+  using SW = SeqSweep<LPU, 4, true, WS>;
+  __shared__ int s_win[(kSeqThreads / LPU) * 2 * SW::WIN];
+  SW st;
+  st.setup_begin(a, s_win);
+  const uint64_t pol = evict_first_policy();
+  const int nnz = a.nnz;
+  const bool cvvec = a.cvvec != 0;
+  const int xoff = (4 * st.gl < st.cm.nt) ? 4 * st.gl : 0;  // idle lanes re-read column 0
+  const char* xg = reinterpret_cast<const char*>(a.X + st.col0 + xoff);
+  const long long xstride = (long long)a.N * 4;
+  const int ea = st.e & ~(B - 1);
+
+  auto load_cv = [&](int eb, int (&c)[B], float (&v)[B]) {
+    if (st.live && cvvec && eb + B <= nnz) {
+#pragma unroll
+      for (int i = 0; i < B; i += 4) {
+        const int4 ci = ld_stream4(a.col + eb + i, pol);
+        const float4 vi = ld_stream4(a.val + eb + i, pol);
+        c[i] = ci.x; c[i + 1] = ci.y; c[i + 2] = ci.z; c[i + 3] = ci.w;
+        v[i] = vi.x; v[i + 1] = vi.y; v[i + 2] = vi.z; v[i + 3] = vi.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const int p = min(eb + j, nnz - 1);
+        const bool ok = st.live && eb + j < nnz;
+        c[j] = ok ? __ldg(a.col + p) : 0;
+        v[j] = ok ? __ldg(a.val + p) : 0.f;
+      }
+    }
+  };
+  auto load_x = [&](const int (&c)[B], float4 (&x)[B]) {
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      x[j] = __ldg(reinterpret_cast<const float4*>(xg + (long long)c[j] * xstride));
+  };
+
+  int cN[B], cNN[B];
+  float vC[B], vN[B], vNN[B];
+  float4 xC[B], xN[B];
+  {
+    int cC[B];
+    load_cv(ea, cC, vC);
+    load_cv(ea + B, cN, vN);
+    st.setup_end(a);
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (ea + j < st.e) vC[j] = 0.f;  // other rows' nonzeros before the unit start
+    load_x(cC, xC);
+  }
+
+#pragma unroll 1
+  for (int eb = ea; __any_sync(0xffffffffu, st.live); eb += B) {
+    load_x(cN, xN);
+    load_cv(eb + 2 * B, cNN, vNN);
+    auto next_bit = [&](int from) -> unsigned {
+      const int d = st.nev - eb;
+      return (st.live && d >= from && d < B) ? (1u << d) : 0u;
+    };
+    unsigned wm = __reduce_or_sync(0xffffffffu, next_bit(0));
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      if (wm & (1u << j)) {  // warp-uniform
+        if (st.live && st.nev == eb + j) st.event(a, eb + j);
+        wm = __reduce_or_sync(0xffffffffu, next_bit(j + 1));
+      }
+      const float v = vC[j];
+      const float4 x = xC[j];
+      if constexpr (EXACT) {
+        st.acc[0] = __fadd_rn(st.acc[0], __fmul_rn(v, x.x));
+        st.acc[1] = __fadd_rn(st.acc[1], __fmul_rn(v, x.y));
+        st.acc[2] = __fadd_rn(st.acc[2], __fmul_rn(v, x.z));
+        st.acc[3] = __fadd_rn(st.acc[3], __fmul_rn(v, x.w));
+      } else {
+        st.acc[0] = fmaf(v, x.x, st.acc[0]);
+        st.acc[1] = fmaf(v, x.y, st.acc[1]);
+        st.acc[2] = fmaf(v, x.z, st.acc[2]);
+        st.acc[3] = fmaf(v, x.w, st.acc[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      xC[j] = xN[j];
+      vC[j] = vN[j];
+      cN[j] = cNN[j];
+      vN[j] = vNN[j];
+    }
+  }
+}
+
+}  // namespace spmk_dev
+
+namespace spmk_dev {
+
+// --------------------------------------------------------------------------
+// seq_async2: the production sequential sweep for 4-aligned column tiles.
+// Dense rows are gathered with cp.async (LDGSTS, 16 B per lane) into an
+// S-stage shared-memory ring (S a power of two), S-1 batches of B nonzeros
+// ahead of consumption; colIdx/val stream through registers S batches ahead
+// (lane gl holds entries gl, gl+LPU, ... of a batch, broadcast by shuffles).
+// The hot loop carries no per-element predicates: positions outside the
+// unit's range read clamped, in-bounds addresses and are never added (values
+// before the unit start are zeroed while acc is +0; the unit stops at its
+// final event).  Events are located per batch with REDUX.OR over the units'
+// next-event bits; the adds run in rounds between event positions, so a
+// batch without events costs one predicated pass.
+// --------------------------------------------------------------------------
+template <int LPU, int B, int S, int NT>
+constexpr int seq_async2_smem_bytes() {
+  return NT * S * B * 16 + (NT / LPU) * 2 * SeqWin<LPU>::WIN * 4;
+}
+
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA = false>
+__global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 1)
+seq_async2_kernel(const SeqArgs a) {
+  static_assert((S & (S - 1)) == 0 && S >= 2, "S must be a power of two");
+  static_assert(B <= 16, "B");
+  constexpr int SLOTS = (B + LPU - 1) / LPU;
+  constexpr unsigned FULL = 0xffffffffu;
+  using SW = SeqSweep<LPU, 4, true, WS, NT>;
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  float4* ring = reinterpret_cast<float4*>(s_dyn);  // [S][B][NT]
+  int* s_win = reinterpret_cast<int*>(s_dyn + NT * S * B * 16);
+  SW st;
+  st.setup_begin(a, s_win);
+  const uint64_t pol = evict_first_policy();
+  const int last = a.nnz - 1;
+  const int xoff = (4 * st.gl < st.cm.nt) ? 4 * st.gl : 0;  // idle lanes re-read column 0
+  const char* xg = reinterpret_cast<const char*>(a.X + st.col0 + xoff);
+  const unsigned xstride = (unsigned)a.N * 4u;
+  const unsigned ring0 = (unsigned)__cvta_generic_to_shared(ring) + threadIdx.x * 16u;
+  const int ea = st.e & ~(B - 1);
+
+  auto load_cv = [&](int eb, int (&c)[SLOTS], float (&v)[SLOTS]) {
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const int o = s * LPU + st.gl;
+      const int p = min(eb + o, last);
+      if (SLOTS * LPU == B || o < B) {
+        c[s] = ld_stream(a.col + p, pol);
+        v[s] = ld_stream(a.val + p, pol);
+      } else {
+        c[s] = 0;
+        v[s] = 0.f;
+      }
+    }
+  };
+  auto issue = [&](int stg, const int (&c)[SLOTS]) {
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const unsigned cj = (unsigned)gshfl<LPU>(c[j / LPU], j % LPU);
+      if constexpr (CA) {
+        cp_async16_ca(ring0 + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)cj * xstride);
+      } else {
+        cp_async16(ring0 + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)cj * xstride);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int cring[S + 1][SLOTS];
+  float vring[S + 1][SLOTS];
+#pragma unroll
+  for (int i = 0; i < S; ++i) load_cv(ea + i * B, cring[i], vring[i]);
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s)
+    if (ea + s * LPU + st.gl < st.e) vring[0][s] = 0.f;  // other rows before the unit start
+  st.setup_end(a);
+#pragma unroll
+  for (int i = 0; i < S - 1; ++i) issue(i, cring[i]);
+
+  int stage = 0;
+#pragma unroll 1
+  for (int eb = ea; __any_sync(FULL, st.live); eb += B) {
+    load_cv(eb + S * B, cring[S], vring[S]);
+    issue((stage + S - 1) & (S - 1), cring[S - 1]);
+    cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
+    const float4* xs = ring + stage * B * NT + threadIdx.x;
+    // products off the add chain (EXACT: rounded product, kernels.hpp:439-441);
+    // fast mode keeps (v, x) and fuses them into the add
+    float pv[B], px[B][4];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const float v = gshfl<LPU>(vring[0][j / LPU], j % LPU);
+      const float4 x = xs[j * NT];
+      if constexpr (EXACT) {
+        px[j][0] = __fmul_rn(v, x.x);
+        px[j][1] = __fmul_rn(v, x.y);
+        px[j][2] = __fmul_rn(v, x.z);
+        px[j][3] = __fmul_rn(v, x.w);
+      } else {
+        px[j][0] = x.x; px[j][1] = x.y; px[j][2] = x.z; px[j][3] = x.w;
+      }
+      pv[j] = v;
+    }
+    auto next_bit = [&](int from) -> unsigned {
+      const int d = st.nev - eb;
+      return (st.live && d >= from && d < B) ? (1u << d) : 0u;
+    };
+    unsigned wm = __reduce_or_sync(FULL, next_bit(0));
+    int js = 0;
+#pragma unroll 1
+    while (true) {
+      const int je = wm ? (__ffs(wm) - 1) : B;
+      const unsigned rng = ((1u << je) - 1u) & ~((1u << js) - 1u);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        if ((rng >> j) & 1u) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            st.acc[k] = EXACT ? __fadd_rn(st.acc[k], px[j][k]) : fmaf(pv[j], px[j][k], st.acc[k]);
+        }
+      }
+      if (je >= B) break;
+      if (st.live && st.nev == eb + je) st.event(a, eb + je);
+      wm = __reduce_or_sync(FULL, next_bit(je + 1));
+      js = je;
+    }
+    stage = (stage + 1) & (S - 1);
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        cring[i][s] = cring[i + 1][s];
+        vring[i][s] = vring[i + 1][s];
       }
   }
   cp_async_wait<0>();

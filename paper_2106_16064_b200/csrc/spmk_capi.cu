@@ -282,28 +282,81 @@ void launch_seq_lpu(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   }
 }
 
-template <int LPU, int B, int S, bool WS>
+template <int LPU, int B, int S, bool WS, int NT>
 void launch_seq_async_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
-  constexpr int smem = seq_async_smem_bytes<LPU, B, S>();
+  constexpr int smem = seq_async_smem_bytes<LPU, B, S, NT>();
   static bool attr_set = false;  // per instantiation (host-side, benign race)
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(seq_kernel_async<LPU, B, S, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(seq_kernel_async<LPU, B, S, WS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
-  const int upb = 256 / LPU;
+  const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq_kernel_async<LPU, B, S, WS><<<grid, 256, smem, s>>>(a);
+  seq_kernel_async<LPU, B, S, WS, NT><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
+}
+
+template <bool WS, int B, int S, int NT>
+void launch_seq_async_nt(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+  switch (lpu) {
+    case 1: launch_seq_async_t<1, B, S, WS, NT>(a, tiles, s); break;
+    case 2: launch_seq_async_t<2, B, S, WS, NT>(a, tiles, s); break;
+    case 4: launch_seq_async_t<4, B, S, WS, NT>(a, tiles, s); break;
+    case 8: launch_seq_async_t<8, B, S, WS, NT>(a, tiles, s); break;
+    case 16: launch_seq_async_t<16, B, S, WS, NT>(a, tiles, s); break;
+    default: launch_seq_async_t<32, B, S, WS, NT>(a, tiles, s); break;
+  }
 }
 
 template <bool WS, int B, int S>
 void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+  const long long nt = env_ll("SPMK_SEQ_NT", 128);
+  if (nt == 64) launch_seq_async_nt<WS, B, S, 64>(a, lpu, tiles, s);
+  else if (nt == 128) launch_seq_async_nt<WS, B, S, 128>(a, lpu, tiles, s);
+  else launch_seq_async_nt<WS, B, S, 256>(a, lpu, tiles, s);
+}
+
+template <int LPU, int B, bool WS, bool EXACT>
+void launch_seq4_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
+  const int upb = 256 / LPU;
+  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
+  seq4_kernel<LPU, B, WS, EXACT><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
+}
+
+template <bool WS, int B, bool EXACT>
+void launch_seq4(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   switch (lpu) {
-    case 1: launch_seq_async_t<1, B, S, WS>(a, tiles, s); break;
-    case 2: launch_seq_async_t<2, B, S, WS>(a, tiles, s); break;
-    case 4: launch_seq_async_t<4, B, S, WS>(a, tiles, s); break;
-    case 8: launch_seq_async_t<8, B, S, WS>(a, tiles, s); break;
-    case 16: launch_seq_async_t<16, B, S, WS>(a, tiles, s); break;
-    default: launch_seq_async_t<32, B, S, WS>(a, tiles, s); break;
+    case 1: launch_seq4_t<1, B, WS, EXACT>(a, tiles, s); break;
+    case 2: launch_seq4_t<2, B, WS, EXACT>(a, tiles, s); break;
+    case 4: launch_seq4_t<4, B, WS, EXACT>(a, tiles, s); break;
+    case 8: launch_seq4_t<8, B, WS, EXACT>(a, tiles, s); break;
+    case 16: launch_seq4_t<16, B, WS, EXACT>(a, tiles, s); break;
+    default: launch_seq4_t<32, B, WS, EXACT>(a, tiles, s); break;
+  }
+}
+
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA>
+void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
+  constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const int upb = NT / LPU;
+  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
+  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
+}
+
+template <bool WS, int B, int S, int NT, bool EXACT, bool CA = false>
+void launch_seq_a2(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+  switch (lpu) {
+    case 1: launch_seq_a2_t<1, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    case 2: launch_seq_a2_t<2, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    case 4: launch_seq_a2_t<4, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    case 8: launch_seq_a2_t<8, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    case 16: launch_seq_a2_t<16, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    default: launch_seq_a2_t<32, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
   }
 }
 
@@ -314,10 +367,27 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     const int lpu = std::min(32, next_pow2(N / 4));
     a.ncol_tile = 4 * lpu;
     const int tiles = (N + a.ncol_tile - 1) / a.ncol_tile;
-    const long long variant = env_ll("SPMK_SEQ_VARIANT", 1);
+    // Measured on B200 (R-MAT s20 heavy/uniform, tools/probe_perf.py): the
+    // lean 2-stage ring wins from 8 lanes per unit up (N >= 32), the 3-stage
+    // ring below.  Other variants stay selectable for experiments.
+    const long long variant = env_ll("SPMK_SEQ_VARIANT", lpu >= 8 ? 9 : 1);
     if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
+    else if (variant == 1) launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
     else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
-    else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
+    else if (variant == 6) launch_seq_async<WS, 8, 4>(a, lpu, tiles, s);
+    else if (variant == 7) launch_seq_async<WS, 4, 4>(a, lpu, tiles, s);
+    else if (variant == 8) launch_seq_a2<WS, 8, 4, 128, true>(a, lpu, tiles, s);
+    else if (variant == 9) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
+    else if (variant == 10) launch_seq_a2<WS, 4, 8, 128, true>(a, lpu, tiles, s);
+    else if (variant == 11) launch_seq_a2<WS, 8, 4, 128, false>(a, lpu, tiles, s);
+    else if (variant == 12) launch_seq_a2<WS, 8, 4, 256, true>(a, lpu, tiles, s);
+    else if (variant == 13) launch_seq_a2<WS, 8, 2, 128, true, true>(a, lpu, tiles, s);
+    else if (variant == 14) launch_seq_a2<WS, 8, 2, 256, true, true>(a, lpu, tiles, s);
+    else if (variant == 15) launch_seq_a2<WS, 8, 2, 256, true>(a, lpu, tiles, s);
+    else if (variant == 16) launch_seq_a2<WS, 16, 2, 128, true>(a, lpu, tiles, s);
+    else if (variant == 4) launch_seq4<WS, 8, false>(a, lpu, tiles, s);
+    else if (variant == 5) launch_seq4<WS, 4, true>(a, lpu, tiles, s);
+    else launch_seq4<WS, 8, true>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
     const int lpu = next_pow2(N / 2);
     a.ncol_tile = 2 * lpu;
@@ -385,7 +455,7 @@ template <int W>
 void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
   const int N = a.N;
   int ct = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : 8;
-  (void)aligned;
+  a.xvec = aligned && ((ct % 4 == 0 && N % 4 == 0) || (ct == 2 && N % 2 == 0));
   a.ncol_tile = ct;
   const int tiles = (N + ct - 1) / ct;
   switch (ct) {
@@ -446,6 +516,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.mne = h->mne;
     a.nnz = (int)h->nnz;
     a.N = N;
+    a.cvvec = ((uintptr_t)h->col % 16 == 0) && ((uintptr_t)h->val % 16 == 0);
     if (id == SPMK_SEQ_ROWSPLIT) {
       const double avg = (double)h->nnz / (double)h->mne;
       int rb = (int)std::lround((double)env_ll("SPMK_SEQ_TILE_NNZ", 256) / std::max(avg, 1.0));
@@ -499,6 +570,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       const long long TS = CH * kParWsChunksPerTile;  // par_ws_kernel tile shape
       Plan& p = get_plan(h, 2, TS, CH, s);
       a.rlo = p.rlo;
+      a.desc = p.desc;
       a.TS = TS;
       a.nunits = (int)p.ntiles;
       if (p.nlong > 0) {

@@ -56,6 +56,26 @@ __global__ void gather_pf(const float* __restrict__ X, const int* __restrict__ i
   if (acc == 12345.f) out[0] = acc;
 }
 
+// 4-byte random gathers: every lane its own index (SpMV x[col] pattern).
+template <int UNROLL>
+__global__ void gather_word(const float* __restrict__ X, const int* __restrict__ idx, long long n,
+                            float* __restrict__ out) {
+  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long nt = (long long)gridDim.x * blockDim.x;
+  float acc = 0.f;
+  for (long long j0 = t; j0 < n; j0 += nt * UNROLL) {
+    int c[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) c[u] = (j0 + u * nt < n) ? __ldg(idx + j0 + u * nt) : 0;
+    float x[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) x[u] = __ldg(X + c[u]);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) acc += x[u];
+  }
+  if (acc == 12345.f) out[0] = acc;
+}
+
 __global__ void fill_idx(int* idx, long long n, long long rows, unsigned long long seed) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     unsigned long long z = seed + i * 0x9e3779b97f4a7c15ULL;
@@ -77,6 +97,21 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
+  for (long long mb : {4LL, 16LL, 64LL}) {  // 4-byte gathers: request rate
+    const long long words = (mb << 20) / 4;
+    fill_idx<<<1184, 256>>>(idx, n, words, 7);
+    for (int blocks : {148 * 8, 148 * 16, 148 * 32}) {
+      gather_word<8><<<blocks, 256>>>(X, idx, n, out);
+      cudaEventRecord(a);
+      for (int r = 0; r < 5; ++r) gather_word<8><<<blocks, 256>>>(X, idx, n, out);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      ms /= 5;
+      printf("x=%5lld MB word gathers blocks=%d  %8.1f us  %7.1f G req/s\n", mb, blocks, ms * 1e3, n / (ms * 1e-3) / 1e9);
+    }
+  }
   for (long long mb : {16LL, 48LL, 96LL, 2048LL}) {
     const long long rows = (mb << 20) / 128;
     fill_idx<<<1184, 256>>>(idx, n, rows, 7);
