@@ -204,6 +204,30 @@ uint64_t spmk_launch_count(void);
 spmk_status spmk_timing_enable(int on);
 spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms);
 
+/* ------------------------------------------------------------ iterative SpMV */
+/* PageRank-style driver support (BASELINE cfg5; no reference counterpart —
+ * the reference has no iterative driver).  With M == K the
+ * column counts are the out-degrees of the transposed graph. */
+/* d_counts[K] = nonzeros per column (deterministic integer atomics). */
+spmk_status spmk_column_counts(spmk_csr_t a, int32_t* d_counts, void* stream);
+/* values[e] = 1 / d_counts[col[e]] (column-stochastic A); the handle must own
+ * its values. */
+spmk_status spmk_csr_values_inv_column_counts(spmk_csr_t a, const int32_t* d_counts,
+                                              void* stream);
+/* doubles of d_scratch the two calls below need */
+int64_t spmk_pagerank_scratch_doubles(void);
+/* d_state[3] = {base, 0, dangling mass of d_r[0..m)} with
+ * base = (1-alpha)/m_total + alpha*dangling/m_total. */
+spmk_status spmk_pagerank_init(const float* d_r, const int32_t* d_counts, int64_t m,
+                               int64_t m_total, double alpha, double* d_state,
+                               double* d_scratch, void* stream);
+/* r[i] = alpha*y[i] + d_state[0] for i < m; then d_state = {next base (from the
+ * local dangling mass), sum|r_new - r_old|, dangling mass}; d_hist[t] = l1
+ * when d_hist is not NULL.  Reductions are fixed-order (bit-reproducible). */
+spmk_status spmk_pagerank_step(const float* d_y, float* d_r, const int32_t* d_counts,
+                               int64_t m, int64_t m_total, double alpha, double* d_state,
+                               double* d_scratch, double* d_hist, int32_t t, void* stream);
+
 /* ------------------------------------------------------------ generators */
 /* generate_rmat<float> (rmat.hpp:61-88 + csr.hpp:123-164) on the device,
  * bit-identical to the reference (counter form of SplitMix64): returns a

@@ -406,3 +406,30 @@ def load_ref():
         return RefLib()
     except (FileNotFoundError, OSError):
         return None
+
+
+# ----------------------------------------------------------------- iterative SpMV
+def pagerank_step64(orc: Oracle, a: Csr, x: np.ndarray, counts: np.ndarray, alpha: float):
+    """One PageRank step in fp64 on the column-stochastic A (a.val already
+    1/outdeg(col)): x' = alpha*A x + (1-alpha)/M + alpha*dangling(x)/M.
+    No reference counterpart (the reference has no iterative driver); this is
+    the checker for paper_2106_16064_b200/pagerank.py.  Returns (x'64, bound)
+    with bound = alpha * sum_j |a_ij x_j| per row."""
+    m = a.m
+    y64, b = orc.oracle_rows(a, x.reshape(m, 1).astype(np.float32))
+    dang = float(np.sum(x.reshape(-1).astype(np.float64)[counts == 0]))
+    base = (1.0 - alpha) / m + alpha * dang / m
+    return alpha * y64[:, 0] + base, alpha * b[:, 0]
+
+
+def pagerank64(orc: Oracle, a: Csr, counts: np.ndarray, alpha: float, iters: int):
+    """fp64 power iteration from x0 = 1/M (free-running reference)."""
+    m = a.m
+    x = np.full(m, 1.0 / m)
+    rows = np.repeat(np.arange(m), np.diff(a.row_ptr))
+    vals = a.val.astype(np.float64)
+    for _ in range(iters):
+        y = np.bincount(rows, weights=vals * x[a.col_idx], minlength=m)
+        dang = x[counts == 0].sum()
+        x = alpha * y + (1.0 - alpha) / m + alpha * dang / m
+    return x

@@ -1,0 +1,109 @@
+// iter_kernels.cuh — iterative SpMV (PageRank-style, BASELINE cfg5) support:
+// column counts (out-degrees of the transposed graph), column-stochastic
+// values, and the per-iteration update with deterministic reductions.
+// None of this is on the reference's path (the reference has no iterative
+// driver); it is the SURVEY §8f row 1 "next" item built on spmm(par-ws).
+#pragma once
+#include <stdint.h>
+
+namespace spmk_dev {
+
+// counts[c] = number of nonzeros in column c (integer atomics: deterministic).
+__global__ void column_counts_kernel(const int* __restrict__ col, long long nnz, int* __restrict__ counts) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    atomicAdd(counts + col[e], 1);
+}
+
+// val[e] = 1 / counts[col[e]]  (column-stochastic A: A x = sum_j x_j / outdeg_j).
+__global__ void inv_count_values_kernel(const int* __restrict__ col, long long nnz,
+                                        const int* __restrict__ counts, float* __restrict__ val) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x)
+    val[e] = 1.0f / (float)counts[col[e]];
+}
+
+// r_new[i] = alpha * y[i] + base, base = st[0] (device scalar).  Per block:
+// partial sums (fp64) of |r_new - r_old| and of r_new over dangling columns
+// (counts == 0), written to part[blockIdx.x * 2 + {0,1}] for the ordered
+// finalize below (no floating-point atomics: run-to-run bit-identical).
+constexpr int kIterThreads = 256;
+__global__ void __launch_bounds__(kIterThreads)
+pagerank_update_kernel(const float* __restrict__ y, float* __restrict__ r, const int* __restrict__ counts,
+                       long long m, float alpha, const double* __restrict__ st, double* __restrict__ part) {
+  __shared__ double s1[kIterThreads / 32], s2[kIterThreads / 32];
+  const float base = (float)st[0];
+  double l1 = 0.0, dang = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float rn = __fadd_rn(__fmul_rn(alpha, y[i]), base);
+    l1 += fabs((double)rn - (double)r[i]);
+    if (counts[i] == 0) dang += (double)rn;
+    r[i] = rn;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    dang += __shfl_xor_sync(0xffffffffu, dang, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s1[threadIdx.x >> 5] = l1;
+    s2[threadIdx.x >> 5] = dang;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kIterThreads / 32; ++w) {
+      a += s1[w];
+      b += s2[w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// Ordered sum of the block partials; st = {base for the next step, l1,
+// dangling mass}; hist[t] = l1 of step t.  One warp, fixed order.
+__global__ void pagerank_finalize_kernel(const double* __restrict__ part, int nblocks, long long m_total,
+                                         double alpha, double* __restrict__ st, double* __restrict__ hist,
+                                         int t) {
+  double l1 = 0.0, dang = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 32) {
+    l1 += part[2 * b];
+    dang += part[2 * b + 1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    dang += __shfl_xor_sync(0xffffffffu, dang, o);
+  }
+  if (threadIdx.x == 0) {
+    st[0] = (1.0 - alpha) / (double)m_total + alpha * dang / (double)m_total;
+    st[1] = l1;
+    st[2] = dang;
+    if (hist) hist[t] = l1;
+  }
+}
+
+// Dangling mass of an initial vector (same ordered reduction).
+__global__ void __launch_bounds__(kIterThreads)
+dangling_mass_kernel(const float* __restrict__ r, const int* __restrict__ counts, long long m,
+                     double* __restrict__ part) {
+  __shared__ double s2[kIterThreads / 32];
+  double dang = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    if (counts[i] == 0) dang += (double)r[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dang += __shfl_xor_sync(0xffffffffu, dang, o);
+  if ((threadIdx.x & 31) == 0) s2[threadIdx.x >> 5] = dang;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < kIterThreads / 32; ++w) b += s2[w];
+    part[2 * blockIdx.x] = 0.0;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+}  // namespace spmk_dev

@@ -19,6 +19,7 @@
 #include "../../include/spmk_capi.h"
 #include "aux_kernels.cuh"
 #include "gen_kernels.cuh"
+#include "iter_kernels.cuh"
 #include "par_kernels.cuh"
 #include "seq_kernels.cuh"
 
@@ -1212,6 +1213,66 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a, d
     if (s) cudaStreamDestroy(s);
     return fail(e.st, e.msg);
   }
+}
+
+// ------------------------------------------------------------ iterative SpMV
+spmk_status spmk_column_counts(spmk_csr_t a, int32_t* d_counts, void* stream) {
+  if (!a || !d_counts) return fail(SPMK_EINVAL, "null argument");
+  DeviceGuard g(a->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  try {
+    CK(cudaMemsetAsync(d_counts, 0, (size_t)a->k * 4, s));
+    if (a->nnz) {
+      column_counts_kernel<<<grid_for(a->nnz), 256, 0, s>>>(a->col, a->nnz, d_counts); LAUNCHED(1);
+    }
+    CK(cudaGetLastError());
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+spmk_status spmk_csr_values_inv_column_counts(spmk_csr_t a, const int32_t* d_counts, void* stream) {
+  if (!a || !d_counts) return fail(SPMK_EINVAL, "null argument");
+  if (!a->own_val) return fail(SPMK_EINVAL, "handle borrows its values; create it with copy=1");
+  DeviceGuard g(a->device);
+  try {
+    if (a->nnz) {
+      inv_count_values_kernel<<<grid_for(a->nnz), 256, 0, (cudaStream_t)stream>>>(a->col, a->nnz, d_counts, a->val);
+      LAUNCHED(1);
+    }
+    CK(cudaGetLastError());
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+  return SPMK_OK;
+}
+
+static const int kIterBlocks = 148 * 8;
+
+int64_t spmk_pagerank_scratch_doubles(void) { return 2 * kIterBlocks; }
+
+spmk_status spmk_pagerank_init(const float* d_r, const int32_t* d_counts, int64_t m, int64_t m_total,
+                               double alpha, double* d_state, double* d_scratch, void* stream) {
+  if (!d_r || !d_counts || !d_state || !d_scratch || m < 0 || m_total < 1) return fail(SPMK_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  dangling_mass_kernel<<<kIterBlocks, kIterThreads, 0, s>>>(d_r, d_counts, m, d_scratch); LAUNCHED(1);
+  pagerank_finalize_kernel<<<1, 32, 0, s>>>(d_scratch, kIterBlocks, m_total, alpha, d_state, nullptr, 0); LAUNCHED(1);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SPMK_OK : fail(SPMK_ECUDA, cudaGetErrorString(e));
+}
+
+spmk_status spmk_pagerank_step(const float* d_y, float* d_r, const int32_t* d_counts, int64_t m,
+                               int64_t m_total, double alpha, double* d_state, double* d_scratch,
+                               double* d_hist, int32_t t, void* stream) {
+  if (!d_y || !d_r || !d_counts || !d_state || !d_scratch || m < 0 || m_total < 1)
+    return fail(SPMK_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  pagerank_update_kernel<<<kIterBlocks, kIterThreads, 0, s>>>(d_y, d_r, d_counts, m, (float)alpha, d_state,
+                                                              d_scratch); LAUNCHED(1);
+  pagerank_finalize_kernel<<<1, 32, 0, s>>>(d_scratch, kIterBlocks, m_total, alpha, d_state, d_hist, t); LAUNCHED(1);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SPMK_OK : fail(SPMK_ECUDA, cudaGetErrorString(e));
 }
 
 uint64_t spmk_launch_count(void) { return g_launches.load(); }

@@ -1,0 +1,289 @@
+"""Selection harness on B200: the reference's measurement / selection-loss
+protocol (proj/include/spmk/bench.hpp) and threshold calibration
+(proj/include/spmk/selector.hpp:36-120), driving the device kernels.
+
+  BenchRecord                bench.hpp:22-33
+  measure_kernel             bench.hpp:65-98   (CUDA events, not steady_clock)
+  run_benchmark              bench.hpp:103-132
+  summarize_selection_loss   bench.hpp:136-189
+  mean_per_n_loss            bench.hpp:191-196
+  min_single_kernel_loss     bench.hpp:198-202
+  emit_csv                   bench.hpp:206-230
+  calibrate_thresholds       selector.hpp:73-120
+
+Device timing: `warmup` discarded calls, then `repeats` calls each bracketed by
+CUDA events on the launching stream, median taken (bench.hpp:74-92).  When
+``flush_l2`` is set a 256 MiB buffer is written before every timed call so
+operands do not start L2-resident.  Correctness ("correct" column) is checked
+on the device without any CPU oracle: every variant must agree with the
+seq-rs result within the north-star bound 1e-5 * (|A| |X|) per element
+(kernels share no code path, so agreement is a real cross-check; the CPU
+oracle parity lives in tests/).
+"""
+from __future__ import annotations
+
+import io
+import math
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+from .spmk import (DeviceCsr, Error, KernelId, MatrixFeatures, SelectorThresholds, kAllKernels,
+                   kernel_index, kernel_name, make_dense_device, parse_kernel, select_kernel)
+
+DENSE_SEED = 0x00D5EED  # bench.hpp:112
+
+
+@dataclass
+class BenchRecord:
+    matrix_name: str
+    num_rows: int = 0
+    num_cols: int = 0
+    nnz: int = 0
+    n: int = 0
+    kernel: str = ""
+    time_seconds: float = 0.0
+    gflops: float = 0.0
+    correct: bool = True
+    selected_by_rule: bool = False
+
+
+@dataclass
+class SelectionLossSummary:
+    per_n_loss: Dict[int, float] = field(default_factory=dict)
+    single_kernel_loss: Dict[str, float] = field(default_factory=dict)
+
+
+# ----------------------------------------------------------------- device timing
+class _Flusher:
+    def __init__(self, device):
+        import torch
+
+        self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    def __call__(self):
+        self.buf.zero_()
+
+
+def _median(v: Sequence[float]) -> float:
+    s = sorted(v)
+    m = len(s) // 2
+    return s[m] if len(s) % 2 == 1 else 0.5 * (s[m - 1] + s[m])
+
+
+def measure_kernel(name: str, a: DeviceCsr, x, kid: KernelId, cfg=None, repeats: int = 7,
+                   warmup: int = 2, flush_l2: bool = True, y=None, stream=None) -> Tuple[BenchRecord, object]:
+    """bench.hpp:65-98 on the device.  Returns (record, y)."""
+    import torch
+
+    if repeats < 1:
+        raise Error("repeats must be >= 1")
+    st = stream or torch.cuda.current_stream(x.device)
+    n = x.shape[1]
+    if y is None:
+        y = torch.empty((a.num_rows, n), dtype=torch.float32, device=x.device)
+    flush = _Flusher(x.device) if flush_l2 else None
+    for _ in range(warmup):
+        a.spmm(kid, x, y, stream=st, cfg=cfg)
+    times = []
+    for _ in range(repeats):
+        if flush:
+            flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        a.spmm(kid, x, y, stream=st, cfg=cfg)
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    t = max(_median(times), 1e-9)
+    rec = BenchRecord(name, a.num_rows, a.num_cols, a.nnz, n, kernel_name(kid), t,
+                      2.0 * a.nnz * n / t / 1e9)
+    return rec, y
+
+
+def _abs_bound(a: DeviceCsr, x):
+    """|A| |X| per element (the north-star tolerance scale), on the device."""
+    import torch
+
+    h = a.download()
+    import numpy as np
+
+    absa = DeviceCsr.from_device(
+        a.num_rows, a.num_cols, torch.from_numpy(h.row_ptr.astype(np.int32)).cuda(x.device),
+        torch.from_numpy(h.col_idx.astype(np.int32)).cuda(x.device),
+        torch.from_numpy(np.abs(h.values)).cuda(x.device), copy=True)
+    return absa.spmm(parse_kernel("seq-rs"), x.abs().contiguous())
+
+
+def run_benchmark(corpus: Iterable[Tuple[str, DeviceCsr]], n_values: Sequence[int], cfg=None,
+                  thresholds: SelectorThresholds = SelectorThresholds(), repeats: int = 7,
+                  warmup: int = 2, flush_l2: bool = True, check: bool = True,
+                  log=None) -> List[BenchRecord]:
+    """bench.hpp:103-132: all four kernels plus the rule-selected one on
+    every (matrix, n) cell; X = make_dense(K, n, 0x00D5EED + n)."""
+    import torch
+
+    corpus = list(corpus)
+    if not corpus:
+        raise Error("run_benchmark: empty corpus")
+    records: List[BenchRecord] = []
+    for name, a in corpus:
+        feats = a.features()
+        for n in n_values:
+            x = make_dense_device(a.num_cols, n, DENSE_SEED + n)
+            ref = bound = None
+            if check:
+                ref = a.spmm(parse_kernel("seq-rs"), x)
+                bound = _abs_bound(a, x)
+            for kid in kAllKernels:
+                rec, y = measure_kernel(name, a, x, kid, cfg, repeats, warmup, flush_l2)
+                if check:
+                    rec.correct = bool(torch.all((y - ref).abs() <= 2e-5 * bound + 1e-30).item())
+                records.append(rec)
+                if log:
+                    log(rec)
+            chosen = select_kernel(feats, n, thresholds)
+            auto = next(r for r in records[-4:] if r.kernel == kernel_name(chosen))
+            arec = BenchRecord(**{**auto.__dict__, "selected_by_rule": True})
+            records.append(arec)
+            del x, ref, bound
+            torch.cuda.empty_cache()
+    return records
+
+
+# ----------------------------------------------------------------- selection loss
+def summarize_selection_loss(records: Sequence[BenchRecord]) -> SelectionLossSummary:
+    """bench.hpp:136-189 — loss = clamp(1 - g/best, 0, 1), best of four per
+    (matrix, n) cell; per-n mean for the rule; per-kernel mean for fixed
+    choices.  Incomplete cells raise."""
+    cells: Dict[Tuple[str, int], dict] = {}
+    for r in records:
+        c = cells.setdefault((r.matrix_name, r.n), {"g": [-1.0] * 4, "auto": -1.0})
+        if r.selected_by_rule:
+            c["auto"] = r.gflops
+        else:
+            c["g"][kernel_index(parse_kernel(r.kernel))] = r.gflops
+    for (m, n), c in sorted(cells.items()):
+        for k in range(4):
+            if c["g"][k] < 0.0:
+                raise Error(f"incomplete records: matrix '{m}' n={n} lacks kernel {kernel_name(kAllKernels[k])}")
+        if c["auto"] < 0.0:
+            raise Error(f"incomplete records: matrix '{m}' n={n} lacks the auto record")
+
+    def loss(g, best):
+        return 0.0 if best <= 0.0 else min(max(1.0 - g / best, 0.0), 1.0)
+
+    s = SelectionLossSummary()
+    count: Dict[int, int] = {}
+    ksum = [0.0] * 4
+    for (m, n), c in sorted(cells.items()):
+        best = max(c["g"])
+        s.per_n_loss[n] = s.per_n_loss.get(n, 0.0) + loss(c["auto"], best)
+        count[n] = count.get(n, 0) + 1
+        for k in range(4):
+            ksum[k] += loss(c["g"][k], best)
+    for n in s.per_n_loss:
+        s.per_n_loss[n] /= count[n]
+    s.per_n_loss = dict(sorted(s.per_n_loss.items()))
+    s.single_kernel_loss = {kernel_name(kAllKernels[k]): ksum[k] / len(cells) for k in range(4)}
+    s.single_kernel_loss = dict(sorted(s.single_kernel_loss.items()))
+    return s
+
+
+def mean_per_n_loss(s: SelectionLossSummary) -> float:
+    return sum(s.per_n_loss.values()) / len(s.per_n_loss) if s.per_n_loss else 0.0
+
+
+def min_single_kernel_loss(s: SelectionLossSummary) -> float:
+    return min([1.0] + list(s.single_kernel_loss.values()))
+
+
+def _fmt(v: float) -> str:
+    return f"{v:.6g}"
+
+
+def emit_csv(records: Sequence[BenchRecord], summary: SelectionLossSummary, out=None) -> str:
+    """bench.hpp:206-230 — same header, same columns, 6 significant digits,
+    the summary as #-prefixed lines."""
+    buf = io.StringIO()
+    buf.write("matrix_name,num_rows,num_cols,nnz,n,kernel,time_seconds,gflops,correct,selected_by_rule\n")
+    for r in records:
+        buf.write(f"{r.matrix_name},{r.num_rows},{r.num_cols},{r.nnz},{r.n},{r.kernel},{_fmt(r.time_seconds)},"
+                  f"{_fmt(r.gflops)},{'true' if r.correct else 'false'},{'true' if r.selected_by_rule else 'false'}\n")
+    for n, l in summary.per_n_loss.items():
+        buf.write(f"# per_n_loss n={n} {_fmt(l)}\n")
+    for k, l in summary.single_kernel_loss.items():
+        buf.write(f"# single_kernel_loss {k} {_fmt(l)}\n")
+    text = buf.getvalue()
+    if out is not None:
+        out.write(text)
+    return text
+
+
+def read_csv(text: str) -> List[BenchRecord]:
+    recs = []
+    for line in text.splitlines()[1:]:
+        if not line or line.startswith("#"):
+            continue
+        f = line.split(",")
+        recs.append(BenchRecord(f[0], int(f[1]), int(f[2]), int(f[3]), int(f[4]), f[5], float(f[6]),
+                                float(f[7]), f[8] == "true", f[9] == "true"))
+    return recs
+
+
+# ----------------------------------------------------------------- calibration
+@dataclass
+class CalibrationRecord:
+    features: MatrixFeatures
+    n: int
+    kernel: KernelId
+    gflops: float
+
+
+def _calibration_loss(cells, t: SelectorThresholds) -> float:
+    total = 0.0
+    for feats, n, g in cells:
+        best = max(g)
+        k = select_kernel(feats, n, t)
+        gk = g[kernel_index(k)]
+        if gk < 0.0:
+            raise Error(f"calibration records lack kernel {kernel_name(k)} for a (matrix, n) cell with n={n}")
+        if best > 0.0:
+            total += max(0.0, 1.0 - gk / best)
+    return total / len(cells)
+
+
+def calibrate_thresholds(records: Sequence[CalibrationRecord]) -> SelectorThresholds:
+    """selector.hpp:73-120: grid search t_parallel_avg in {8..128} x t_cv in
+    {0.25..4} for the lowest mean loss; ties toward the defaults (log2
+    distance); n_parallel_max kept."""
+    if not records:
+        raise Error("calibrate_thresholds: empty record list")
+    grouped: Dict[tuple, list] = {}
+    for r in records:
+        f = r.features
+        key = (f.num_rows, f.nnz, f.avg_row, f.stdv_row, r.n)
+        cell = grouped.setdefault(key, [f, r.n, [-1.0] * 4])
+        cell[0] = f
+        cell[2][kernel_index(r.kernel)] = r.gflops
+    cells = []
+    for key in sorted(grouped):
+        f, n, g = grouped[key]
+        if sum(1 for v in g if v >= 0.0) < 2:
+            raise Error("calibration requires >= 2 kernels per (matrix, n) pair")
+        cells.append((f, n, g))
+    d = SelectorThresholds()
+    best, best_loss, best_dist = d, _calibration_loss(cells, d), 0.0
+    for tp in (8.0, 16.0, 32.0, 64.0, 128.0):
+        for tc in (0.25, 0.5, 1.0, 2.0, 4.0):
+            cand = SelectorThresholds(d.n_parallel_max, tp, tc)
+            l = _calibration_loss(cells, cand)
+            dist = abs(math.log2(tp / d.t_parallel_avg)) + abs(math.log2(tc / d.t_cv))
+            if l < best_loss - 1e-12 or (l < best_loss + 1e-12 and dist < best_dist):
+                best, best_loss, best_dist = cand, l, dist
+    return best
+
+
+def calibration_records(records: Sequence[BenchRecord], features: Dict[str, MatrixFeatures]):
+    """BenchRecords (non-auto) -> CalibrationRecords (bench_main.cpp:101-113)."""
+    return [CalibrationRecord(features[r.matrix_name], r.n, parse_kernel(r.kernel), r.gflops)
+            for r in records if not r.selected_by_rule]

@@ -91,6 +91,11 @@ _SIGS = {
     "spmk_timing_last": ([P(f32), P(f32)], C.c_int),
     "spmk_generate_rmat": ([C.c_uint32, u64, f64, f64, f64, f64, u64, C.c_int, P(vp)], C.c_int),
     "spmk_make_dense": ([i64, i64, u64, vp, vp], C.c_int),
+    "spmk_column_counts": ([vp, vp, vp], C.c_int),
+    "spmk_csr_values_inv_column_counts": ([vp, vp, vp], C.c_int),
+    "spmk_pagerank_scratch_doubles": ([], i64),
+    "spmk_pagerank_init": ([vp, vp, i64, i64, f64, vp, vp, vp], C.c_int),
+    "spmk_pagerank_step": ([vp, vp, vp, i64, i64, f64, vp, vp, vp, C.c_int32, vp], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

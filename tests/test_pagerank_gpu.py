@@ -1,0 +1,86 @@
+"""Iterative SpMV (PageRank-style, BASELINE cfg5 workload) on the device vs
+the fp64 oracle: teacher-forced steps within the north-star bound, the
+free-running iteration within eps/(1-alpha), graph replay bit-identical to
+eager steps, residual history monotone."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2106_16064_b200 as spmk  # noqa: E402
+from oracle.oracle import Csr, pagerank64, pagerank_step64  # noqa: E402
+from paper_2106_16064_b200 import pagerank as prk  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+ALPHA = 0.85
+
+
+def host(d):
+    h = d.download()
+    return Csr(h.num_rows, h.num_cols, h.row_ptr, h.col_idx, h.values)
+
+
+@pytest.fixture(scope="module")
+def graph():
+    d = spmk.DeviceCsr.generate_rmat(12, 8, (0.57, 0.19, 0.19, 0.05), 3)
+    pr = prk.PageRank(d, ALPHA)
+    torch.cuda.synchronize()
+    return d, pr, host(d), pr.counts.cpu().numpy()
+
+
+def test_column_stochastic_values(graph):
+    d, pr, a, counts = graph
+    assert np.array_equal(counts, np.bincount(a.col_idx, minlength=a.k))
+    want = (np.float32(1.0) / counts[a.col_idx].astype(np.float32)).astype(np.float32)
+    assert np.array_equal(a.val, want)
+    assert pr.kid == d.select(1)
+
+
+def test_teacher_forced_steps(graph, orc):
+    d, pr, a, counts = graph
+    pr.reset()
+    for t in range(3):
+        x = pr.x.cpu().numpy().reshape(-1).copy()
+        pr.step()
+        got = pr.x.cpu().numpy().reshape(-1).astype(np.float64)
+        want, bound = pagerank_step64(orc, a, x, counts, ALPHA)
+        # SpMV within 1e-5*sum|a x| (north_star), plus the fp32 rounding of the update
+        assert np.all(np.abs(got - want) <= 1e-5 * bound + 2e-7 * np.abs(want)), f"step {t}"
+        st = pr.state.cpu().numpy()
+        assert st[1] == pytest.approx(np.abs(got - x).sum(), rel=1e-6)
+
+
+def test_free_running_and_graph_replay(graph, orc):
+    d, pr, a, counts = graph
+    iters = 30
+    x_eager, h_eager = pr.run(iters, graph=False)
+    x_eager = x_eager.cpu().numpy().copy()
+    h_eager = h_eager.cpu().numpy().copy()
+    x_graph, h_graph = pr.run(iters, graph=True)
+    assert np.array_equal(x_graph.cpu().numpy(), x_eager), "graph replay must equal eager steps"
+    assert np.array_equal(h_graph.cpu().numpy(), h_eager)
+    ref = pagerank64(orc, a, counts, ALPHA, iters)
+    assert np.abs(x_eager.reshape(-1) - ref).sum() <= 1e-5 / (1 - ALPHA)
+    assert abs(x_eager.sum() - 1.0) < 1e-4
+    assert np.all(np.diff(h_eager[2:]) <= 1e-12)  # contraction after the first steps
+
+
+def test_distributed_driver_single_rank_matches(graph, orc):
+    """The multi-GPU driver at world_size 1 (gloo-free path: 1-rank NCCL group)
+    computes the same iteration as the single-GPU driver."""
+    import os
+
+    import torch.distributed as dist
+
+    d, pr, a, counts = graph
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        d2 = spmk.DeviceCsr.generate_rmat(12, 8, (0.57, 0.19, 0.19, 0.05), 3)
+        dp = prk.DistributedPageRank(d2, ALPHA)
+        x, _ = dp.run(10)
+        x1, _ = pr.run(10, graph=False)
+        assert np.array_equal(x.cpu().numpy(), x1.cpu().numpy())
+    finally:
+        dist.destroy_process_group()
