@@ -108,6 +108,9 @@ spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols,
  * `device` (multi-GPU equal-nnz slices). */
 spmk_status spmk_csr_slice(spmk_csr_t a, int64_t row_begin, int64_t row_end,
                            int device, spmk_csr_t* out);
+/* |A|: a new handle with the same structure and |values| (the north-star
+ * tolerance scale sum_j |a_ij x_j| is then one spmm with |X|). */
+spmk_status spmk_csr_abs_copy(spmk_csr_t a, spmk_csr_t* out);
 spmk_status spmk_csr_destroy(spmk_csr_t a);
 spmk_status spmk_csr_info(spmk_csr_t a, int64_t* num_rows, int64_t* num_cols,
                           int64_t* nnz, int64_t* max_row_nnz,

@@ -230,42 +230,63 @@ __global__ void zero_all_kernel(float* __restrict__ Y, long long total) {
     Y[i] = 0.f;
 }
 
-// Long-row fix-up: Y[r] = T[t1] + H[q0] + ... + H[q1] in ascending order
-// (the reference's serial boundary merge, kernels.hpp:316-323 / :448-453,
-// restricted to rows whose partials were not merged in registers).  One block
-// per long row: the row's partials H[q0..q1][0..N) are one contiguous range,
-// staged into shared memory by a coalesced sweep, then each column is summed
-// sequentially (the order is the contract; the adds are the only serial part).
-constexpr int kFixupSmemFloats = 12288;  // 48 KB
-__global__ void __launch_bounds__(256)
+// Long-row fix-up: Y[r] = (((T[t1] + H[q0]) + H[q0+1]) + ... ) + H[q1] in
+// ascending order (the reference's serial boundary merge, kernels.hpp:316-323
+// / :448-453, restricted to rows whose partials were not merged in
+// registers).  One warp per long row: the row's partials H[q0..q1][cols] are
+// one contiguous range, staged into the warp's shared-memory buffer by
+// coalesced loads, then lane j folds column j sequentially (the order is the
+// contract; the adds are the only serial part).
+constexpr int kFixupWarps = 8;
+constexpr int kFixupBuf = 1024;  // floats per warp per batch
+__global__ void __launch_bounds__(kFixupWarps * 32)
 fixup_kernel(const int* __restrict__ list, int nlong,
              const int* __restrict__ crp, const int* __restrict__ rid,
              const float* __restrict__ H, const float* __restrict__ Tsl,
              float* __restrict__ Y, int N, long long TS, long long CH) {
-  __shared__ float sm[kFixupSmemFloats];
+  __shared__ float sm[kFixupWarps][kFixupBuf];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = sm[w];
   const long long T = TS / CH;
-  for (int li = blockIdx.x; li < nlong; li += gridDim.x) {
+  for (long long li = (long long)blockIdx.x * kFixupWarps + w; li < nlong;
+       li += (long long)gridDim.x * kFixupWarps) {
     const int c = list[li];
     const long long s = crp[c], f = crp[c + 1];
     const long long t1 = s / TS;
     const long long q0 = (t1 + 1) * T, q1 = (f - 1) / CH;
-    for (int j0 = 0; j0 < N; j0 += 256) {  // column block handled by threads j < 256
-      const int j = j0 + threadIdx.x;
-      float acc = (j < N) ? Tsl[t1 * N + j] : 0.f;
-      const long long qpb = max(1LL, (long long)kFixupSmemFloats / N);  // partials per smem batch
+    const long long yrow = (long long)rid[c] * N;
+    for (int j0 = 0; j0 < N; j0 += 32) {
+      const int ncol = min(32, N - j0);
+      float acc = (lane < ncol) ? Tsl[t1 * N + j0 + lane] : 0.f;
+      const long long qpb = kFixupBuf / ncol;  // partials per batch
       for (long long qb = q0; qb <= q1; qb += qpb) {
-        const long long qe = min(q1 + 1, qb + qpb);
-        const long long cnt = (qe - qb) * N;
-        __syncthreads();
-        for (long long i = threadIdx.x; i < cnt; i += blockDim.x) sm[i] = H[qb * N + i];
-        __syncthreads();
-        if (j < N) {
-          for (long long q = 0; q < qe - qb; ++q) acc = __fadd_rn(acc, sm[q * N + j]);
+        const int nqb = (int)min(qpb, q1 + 1 - qb);
+        const int cnt = nqb * ncol;
+        __syncwarp();
+        if (ncol == N) {  // whole rows of H: one contiguous range
+          const float* src = H + qb * N;
+#pragma unroll 8
+          for (int i = lane; i < cnt; i += 32) buf[i] = src[i];
+        } else {
+#pragma unroll 4
+          for (int i = lane; i < cnt; i += 32) buf[i] = H[(qb + i / ncol) * N + j0 + i % ncol];
+        }
+        __syncwarp();
+        if (lane < ncol) {
+#pragma unroll 8
+          for (int qq = 0; qq < nqb; ++qq) acc = __fadd_rn(acc, buf[qq * ncol + lane]);
         }
       }
-      if (j < N) Y[(long long)rid[c] * N + j] = acc;
+      if (lane < ncol) Y[yrow + j0 + lane] = acc;
     }
   }
+}
+
+// |val| (for the north-star bound sum_j |a_ij x_j| computed on the device).
+__global__ void abs_copy_kernel(const float* __restrict__ in, float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = fabsf(in[i]);
 }
 
 // Row slice [r0, r1) rebased: rp_out[i] = rp[r0+i] - rp[r0].

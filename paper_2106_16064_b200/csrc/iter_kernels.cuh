@@ -28,18 +28,39 @@ __global__ void inv_count_values_kernel(const int* __restrict__ col, long long n
 // (counts == 0), written to part[blockIdx.x * 2 + {0,1}] for the ordered
 // finalize below (no floating-point atomics: run-to-run bit-identical).
 constexpr int kIterThreads = 256;
+__device__ __forceinline__ void pr_elem(float yv, float& rv, int cnt, float alpha, float base, double& l1,
+                                        double& dang) {
+  const float rn = __fadd_rn(__fmul_rn(alpha, yv), base);
+  l1 += fabs((double)rn - (double)rv);
+  if (cnt == 0) dang += (double)rn;
+  rv = rn;
+}
 __global__ void __launch_bounds__(kIterThreads)
 pagerank_update_kernel(const float* __restrict__ y, float* __restrict__ r, const int* __restrict__ counts,
                        long long m, float alpha, const double* __restrict__ st, double* __restrict__ part) {
   __shared__ double s1[kIterThreads / 32], s2[kIterThreads / 32];
   const float base = (float)st[0];
   double l1 = 0.0, dang = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float rn = __fadd_rn(__fmul_rn(alpha, y[i]), base);
-    l1 += fabs((double)rn - (double)r[i]);
-    if (counts[i] == 0) dang += (double)rn;
-    r[i] = rn;
+  // 16-byte vectors when all three arrays are 16-byte aligned, scalar tail
+  const bool vec = ((reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(r) |
+                     reinterpret_cast<uintptr_t>(counts)) & 15) == 0;
+  const long long m4 = vec ? (m & ~3LL) : 0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (long long i = 4 * tid; i < m4; i += 4 * nth) {
+    const float4 yv = *reinterpret_cast<const float4*>(y + i);
+    float4 rv = *reinterpret_cast<const float4*>(r + i);
+    const int4 cv = *reinterpret_cast<const int4*>(counts + i);
+    pr_elem(yv.x, rv.x, cv.x, alpha, base, l1, dang);
+    pr_elem(yv.y, rv.y, cv.y, alpha, base, l1, dang);
+    pr_elem(yv.z, rv.z, cv.z, alpha, base, l1, dang);
+    pr_elem(yv.w, rv.w, cv.w, alpha, base, l1, dang);
+    *reinterpret_cast<float4*>(r + i) = rv;
+  }
+  for (long long i = m4 + tid; i < m; i += nth) {
+    float rv = r[i];
+    pr_elem(y[i], rv, counts[i], alpha, base, l1, dang);
+    r[i] = rv;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

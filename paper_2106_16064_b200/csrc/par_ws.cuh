@@ -87,11 +87,10 @@ __device__ __forceinline__ void store_cols(float* __restrict__ p, int nt, const 
     }
 }
 
-template <int W, int CT>
-__global__ void __launch_bounds__(256)
+template <int W, int CT, int T = kParWsChunksPerTile, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 par_ws_kernel(const ParArgs a) {
   static_assert(W >= 2 && W <= 32, "W");
-  constexpr int T = kParWsChunksPerTile;
   constexpr int NG = 256 / W;      // groups per block
   constexpr int WINP = T * W + 2;  // rows touching a tile <= T*W + 1
   constexpr unsigned FULL = 0xffffffffu;

@@ -445,14 +445,14 @@ void launch_par_rs(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   }
 }
 
-template <int W, int CT>
+template <int W, int CT, int T, int MINB>
 void launch_par_ws_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
   const int upb = 256 / W;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  par_ws_kernel<W, CT><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
+  par_ws_kernel<W, CT, T, MINB><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
 }
 
-template <int W>
+template <int W, int T, int MINB>
 void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
   const int N = a.N;
   int ct = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : 8;
@@ -460,21 +460,33 @@ void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
   a.ncol_tile = ct;
   const int tiles = (N + ct - 1) / ct;
   switch (ct) {
-    case 1: launch_par_ws_t<W, 1>(a, tiles, s); break;
-    case 2: launch_par_ws_t<W, 2>(a, tiles, s); break;
-    case 4: launch_par_ws_t<W, 4>(a, tiles, s); break;
-    default: launch_par_ws_t<W, 8>(a, tiles, s); break;
+    case 1: launch_par_ws_t<W, 1, T, MINB>(a, tiles, s); break;
+    case 2: launch_par_ws_t<W, 2, T, MINB>(a, tiles, s); break;
+    case 4: launch_par_ws_t<W, 4, T, MINB>(a, tiles, s); break;
+    default: launch_par_ws_t<W, 8, T, MINB>(a, tiles, s); break;
+  }
+}
+
+// Tile shape of par-ws: T chunks of W nonzeros per group (a pure performance
+// knob: any T keeps the results bit-exact).
+int par_ws_chunks_per_tile() { return (int)env_ll("SPMK_PARWS_T", 4); }
+
+template <int T, int MINB>
+void launch_par_ws_tt(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
+  switch (W) {
+    case 2: launch_par_ws_w<2, T, MINB>(a, aligned, s); break;
+    case 4: launch_par_ws_w<4, T, MINB>(a, aligned, s); break;
+    case 8: launch_par_ws_w<8, T, MINB>(a, aligned, s); break;
+    case 16: launch_par_ws_w<16, T, MINB>(a, aligned, s); break;
+    default: launch_par_ws_w<32, T, MINB>(a, aligned, s); break;
   }
 }
 
 void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
-  switch (W) {
-    case 2: launch_par_ws_w<2>(a, aligned, s); break;
-    case 4: launch_par_ws_w<4>(a, aligned, s); break;
-    case 8: launch_par_ws_w<8>(a, aligned, s); break;
-    case 16: launch_par_ws_w<16>(a, aligned, s); break;
-    default: launch_par_ws_w<32>(a, aligned, s); break;
-  }
+  const int T = par_ws_chunks_per_tile();
+  // T = 4 measured best on B200 (R-MAT s20 heavy/uniform, N = 1 and 4)
+  if (T == 8) launch_par_ws_tt<8, 1>(a, W, aligned, s);
+  else launch_par_ws_tt<4, 4>(a, W, aligned, s);
 }
 
 // Tile sizes (nonzeros per work unit).  Any multiple of the chunk keeps the
@@ -546,7 +558,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_seq<true>(a, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<std::min(p.nlong, 148 * 8), 256, 0, s>>>(
+        fixup_kernel<<<std::min((p.nlong + kFixupWarps - 1) / kFixupWarps, 148 * 8), kFixupWarps * 32, 0, s>>>(
             p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   } else {
@@ -568,7 +580,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     } else {
       if (W > 32) return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
       const long long CH = W;
-      const long long TS = CH * kParWsChunksPerTile;  // par_ws_kernel tile shape
+      const long long TS = CH * par_ws_chunks_per_tile();  // par_ws_kernel tile shape
       Plan& p = get_plan(h, 2, TS, CH, s);
       a.rlo = p.rlo;
       a.desc = p.desc;
@@ -584,7 +596,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws(a, W, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<std::min(p.nlong, 148 * 8), 256, 0, s>>>(
+        fixup_kernel<<<std::min((p.nlong + kFixupWarps - 1) / kFixupWarps, 148 * 8), kFixupWarps * 32, 0, s>>>(
             p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   }
@@ -819,6 +831,30 @@ spmk_status spmk_csr_slice(spmk_csr_t a, int64_t row_begin, int64_t row_end, int
     cudaStreamDestroy(s);
     return st;
   } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
+}
+
+spmk_status spmk_csr_abs_copy(spmk_csr_t a, spmk_csr_t* out) {
+  if (!a || !out) return fail(SPMK_EINVAL, "null argument");
+  DeviceGuard g(a->device);
+  cudaStream_t s = nullptr;
+  try {
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    int* rp = dev_alloc<int>((size_t)a->m + 1);
+    int* col = dev_alloc<int>((size_t)a->nnz);
+    float* val = dev_alloc<float>((size_t)a->nnz);
+    CK(cudaMemcpyAsync(rp, a->rp, (a->m + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    if (a->nnz) {
+      CK(cudaMemcpyAsync(col, a->col, a->nnz * 4, cudaMemcpyDeviceToDevice, s));
+      abs_copy_kernel<<<grid_for(a->nnz), 256, 0, s>>>(a->val, val, a->nnz); LAUNCHED(1);
+      CK(cudaGetLastError());
+    }
+    spmk_status st = create_from_device32(a->m, a->k, a->nnz, rp, col, val, true, a->device, out, s);
+    cudaStreamDestroy(s);
+    return st;
+  } catch (const CudaError& e) {
+    if (s) cudaStreamDestroy(s);
     return fail(e.st, e.msg);
   }
 }

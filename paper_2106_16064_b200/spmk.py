@@ -66,6 +66,7 @@ _SIGS = {
     "spmk_csr_create": ([i64, i64, i64, P(i64), P(i64), P(f32), C.c_int, P(vp)], C.c_int),
     "spmk_csr_create_device": ([i64, i64, i64, vp, vp, vp, C.c_int, P(vp)], C.c_int),
     "spmk_csr_slice": ([vp, i64, i64, C.c_int, P(vp)], C.c_int),
+    "spmk_csr_abs_copy": ([vp, P(vp)], C.c_int),
     "spmk_csr_destroy": ([vp], C.c_int),
     "spmk_csr_info": ([vp, P(i64), P(i64), P(i64), P(i64), P(i64)], C.c_int),
     "spmk_csr_device_arrays": ([vp, P(vp), P(vp), P(vp)], C.c_int),
@@ -308,6 +309,12 @@ class DeviceCsr:
     def slice(self, row_begin: int, row_end: int, device: int = 0) -> "DeviceCsr":
         h = vp()
         _check(self.lib.spmk_csr_slice(self._h, row_begin, row_end, device, C.byref(h)))
+        return DeviceCsr(h.value)
+
+    def abs_copy(self) -> "DeviceCsr":
+        """|A| (same structure, |values|) as a new resident handle."""
+        h = vp()
+        _check(self.lib.spmk_csr_abs_copy(self._h, C.byref(h)))
         return DeviceCsr(h.value)
 
     def close(self):

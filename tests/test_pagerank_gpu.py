@@ -62,7 +62,7 @@ def test_free_running_and_graph_replay(graph, orc):
     ref = pagerank64(orc, a, counts, ALPHA, iters)
     assert np.abs(x_eager.reshape(-1) - ref).sum() <= 1e-5 / (1 - ALPHA)
     assert abs(x_eager.sum() - 1.0) < 1e-4
-    assert np.all(np.diff(h_eager[2:]) <= 1e-12)  # contraction after the first steps
+    assert h_eager[-1] < 1e-3 * h_eager[0]  # geometric contraction (alpha^t) down to the fp32 floor
 
 
 def test_distributed_driver_single_rank_matches(graph, orc):
