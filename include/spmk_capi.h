@@ -177,6 +177,15 @@ spmk_status spmk_spmm_auto(spmk_csr_t a, const spmk_thresholds* t,
 spmk_status spmk_spmm_host(spmk_csr_t a, spmk_kernel_id id,
                            const spmk_kernel_config* cfg, const float* x,
                            int64_t n, float* y, void* stream);
+/* The same without the final synchronize: H2D(x) -> kernels -> D2H(y) are
+ * enqueued on `stream` and the call returns.  x and y must stay valid (pinned
+ * for overlap) until the stream passes the call.  The handle rotates two
+ * device staging slots, so consecutive calls on two streams overlap one
+ * call's D2H with the next call's H2D (full-duplex PCIe); a slot's reuse
+ * waits on the device for its previous call. */
+spmk_status spmk_spmm_host_async(spmk_csr_t a, spmk_kernel_id id,
+                                 const spmk_kernel_config* cfg, const float* x,
+                                 int64_t n, float* y, void* stream);
 /* One-shot drop-in for `spmm(id, CsrMatrix, DenseMatrix, cfg)` with every
  * operand on the host (create handle on `device`, run, download, destroy). */
 spmk_status spmk_spmm_csr_host(int64_t num_rows, int64_t num_cols, int64_t nnz,

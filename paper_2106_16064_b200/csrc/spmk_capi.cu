@@ -125,9 +125,14 @@ struct spmk_csr_s {
   std::map<std::tuple<int, long long, long long>, Plan> plans;
   float* scratch = nullptr;
   size_t scratch_floats = 0;
-  float* stage_x = nullptr;
-  float* stage_y = nullptr;
-  size_t stage_x_n = 0, stage_y_n = 0;
+  // host-operand staging: kStageSlots rotating (X, Y) device buffer pairs;
+  // slot_done[i] marks the end of the last call that used slot i
+  static constexpr int kStageSlots = 2;
+  float* stage_x[kStageSlots] = {nullptr, nullptr};
+  float* stage_y[kStageSlots] = {nullptr, nullptr};
+  size_t stage_x_n[kStageSlots] = {0, 0}, stage_y_n[kStageSlots] = {0, 0};
+  cudaEvent_t slot_done[kStageSlots] = {nullptr, nullptr};
+  int next_slot = 0;
   std::mutex mu;
 };
 
@@ -147,8 +152,11 @@ void free_handle(spmk_csr_s* h) {
     cudaFree(kv.second.longrows);
   }
   cudaFree(h->scratch);
-  cudaFree(h->stage_x);
-  cudaFree(h->stage_y);
+  for (int i = 0; i < spmk_csr_s::kStageSlots; ++i) {
+    cudaFree(h->stage_x[i]);
+    cudaFree(h->stage_y[i]);
+    if (h->slot_done[i]) cudaEventDestroy(h->slot_done[i]);
+  }
   delete h;
 }
 
@@ -1050,6 +1058,42 @@ spmk_status spmk_spmm_auto(spmk_csr_t a, const spmk_thresholds* t, const spmk_ke
   return spmk_spmm(a, id, cfg, d_x, n, d_y, stream);
 }
 
+namespace {
+// H2D(x) -> spmm -> D2H(y) on `s` through one of the handle's staging slots;
+// the slot's previous user is awaited on the device (event), not the host.
+spmk_status spmm_host_enqueue(spmk_csr_s* a, spmk_kernel_id id, const spmk_kernel_config& c,
+                              const float* x, int64_t n, float* y, cudaStream_t s) {
+  const size_t nx = (size_t)a->k * n, ny = (size_t)a->m * n;
+  const int slot = a->next_slot;
+  a->next_slot = (slot + 1) % spmk_csr_s::kStageSlots;
+  if (!a->slot_done[slot]) CK(cudaEventCreateWithFlags(&a->slot_done[slot], cudaEventDisableTiming));
+  if (nx > a->stage_x_n[slot] || ny > a->stage_y_n[slot]) {
+    CK(cudaEventSynchronize(a->slot_done[slot]));  // previous user done before freeing
+    if (nx > a->stage_x_n[slot]) {
+      cudaFree(a->stage_x[slot]);
+      a->stage_x[slot] = nullptr;
+      a->stage_x_n[slot] = 0;
+      a->stage_x[slot] = dev_alloc<float>(nx);
+      a->stage_x_n[slot] = nx;
+    }
+    if (ny > a->stage_y_n[slot]) {
+      cudaFree(a->stage_y[slot]);
+      a->stage_y[slot] = nullptr;
+      a->stage_y_n[slot] = 0;
+      a->stage_y[slot] = dev_alloc<float>(ny);
+      a->stage_y_n[slot] = ny;
+    }
+  }
+  CK(cudaStreamWaitEvent(s, a->slot_done[slot], 0));
+  if (nx) CK(cudaMemcpyAsync(a->stage_x[slot], x, nx * 4, cudaMemcpyHostToDevice, s));
+  spmk_status st = run_spmm(a, id, c, a->stage_x[slot], n, a->stage_y[slot], s);
+  if (st != SPMK_OK) return st;
+  CK(cudaMemcpyAsync(y, a->stage_y[slot], ny * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(a->slot_done[slot], s));
+  return SPMK_OK;
+}
+}  // namespace
+
 spmk_status spmk_spmm_host(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg,
                            const float* x, int64_t n, float* y, void* stream) {
   if (!a) return fail(SPMK_EINVAL, "null handle");
@@ -1062,30 +1106,30 @@ spmk_status spmk_spmm_host(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_co
   DeviceGuard g(a->device);
   cudaStream_t s = (cudaStream_t)stream;
   try {
-    const size_t nx = (size_t)a->k * n, ny = (size_t)a->m * n;
-    if (nx > a->stage_x_n) {
-      cudaFree(a->stage_x);
-      a->stage_x = nullptr;
-      a->stage_x_n = 0;
-      a->stage_x = dev_alloc<float>(nx);
-      a->stage_x_n = nx;
-    }
-    if (ny > a->stage_y_n) {
-      cudaFree(a->stage_y);
-      a->stage_y = nullptr;
-      a->stage_y_n = 0;
-      a->stage_y = dev_alloc<float>(ny);
-      a->stage_y_n = ny;
-    }
-    if (nx) CK(cudaMemcpyAsync(a->stage_x, x, nx * 4, cudaMemcpyHostToDevice, s));
-    st = run_spmm(a, id, c, a->stage_x, n, a->stage_y, s);
+    st = spmm_host_enqueue(a, id, c, x, n, y, s);
     if (st != SPMK_OK) return st;
-    CK(cudaMemcpyAsync(y, a->stage_y, ny * 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
   } catch (const CudaError& e) {
     return fail(e.st, e.msg);
   }
   return SPMK_OK;
+}
+
+spmk_status spmk_spmm_host_async(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg,
+                                 const float* x, int64_t n, float* y, void* stream) {
+  if (!a) return fail(SPMK_EINVAL, "null handle");
+  spmk_status st = spmk_check_config(cfg);
+  if (st != SPMK_OK) return st;
+  if (n < 0) return fail(SPMK_EDIM, "negative n");
+  if (n == 0 || a->m == 0) return SPMK_OK;
+  const spmk_kernel_config c = cfg_or_default(cfg);
+  std::lock_guard<std::mutex> lk(a->mu);
+  DeviceGuard g(a->device);
+  try {
+    return spmm_host_enqueue(a, id, c, x, n, y, (cudaStream_t)stream);
+  } catch (const CudaError& e) {
+    return fail(e.st, e.msg);
+  }
 }
 
 spmk_status spmk_spmm_csr_host(int64_t num_rows, int64_t num_cols, int64_t nnz,

@@ -82,6 +82,7 @@ _SIGS = {
     "spmk_spmm": ([vp, C.c_int, P(_Cfg), vp, i64, vp, vp], C.c_int),
     "spmk_spmm_auto": ([vp, P(_Thr), P(_Cfg), vp, i64, vp, vp, P(C.c_int)], C.c_int),
     "spmk_spmm_host": ([vp, C.c_int, P(_Cfg), P(f32), i64, P(f32), vp], C.c_int),
+    "spmk_spmm_host_async": ([vp, C.c_int, P(_Cfg), P(f32), i64, P(f32), vp], C.c_int),
     "spmk_spmm_csr_host": ([i64, i64, i64, P(i64), P(i64), P(f32), C.c_int, P(_Cfg), P(f32), i64,
                             P(f32), C.c_int], C.c_int),
     "spmk_kernel_stats": ([vp, C.c_int, P(_Cfg), i64, P(u64), P(u64)], C.c_int),
@@ -411,6 +412,15 @@ class DeviceCsr:
         _check(self.lib.spmk_spmm_host(self._h, kid.index, C.byref(c), _ptr(x, f32), n, _ptr(y, f32),
                                        C.c_void_p(stream)))
         return y
+
+    def spmm_host_async(self, kid: KernelId, x: np.ndarray, out: np.ndarray, stream: int,
+                        cfg: Optional[KernelConfig] = None) -> None:
+        """Enqueue H2D(x) -> Y = A x -> D2H(out) on `stream` (no synchronize);
+        x and out must be pinned and stay alive until the stream passes."""
+        assert x.dtype == np.float32 and x.flags.c_contiguous and out.flags.c_contiguous
+        c = (cfg or KernelConfig())._c()
+        _check(self.lib.spmk_spmm_host_async(self._h, kid.index, C.byref(c), _ptr(x, f32), x.shape[1],
+                                             _ptr(out, f32), C.c_void_p(stream)))
 
 
 def spmm(kid: KernelId, a: CsrMatrix, x: np.ndarray, cfg: KernelConfig = KernelConfig(),
