@@ -197,11 +197,14 @@ def main():
 
     ws, rank, local = dist_env()
     G = max(ws, 1)
-    if args.gpus != G and ws > 1:
+    # torchrun (any world size, including 1) runs the distributed code path:
+    # NCCL process group, equal-nnz slicing, X broadcast, max-over-ranks.
+    use_dist = "WORLD_SIZE" in os.environ
+    if args.gpus != G and use_dist:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
 
     n = args.n
@@ -209,7 +212,7 @@ def main():
     assert 1 << (scale - args.scale) == G, "--gpus must be a power of two"
     t0 = time.time()
     full = spmk.DeviceCsr.generate_rmat(scale, args.edge_factor, HEAVY, 1, device=local)
-    if G > 1:
+    if use_dist:
         bounds = full.row_slices(G)
         a = full.slice(int(bounds[rank]), int(bounds[rank + 1]), device=local)
         del full
@@ -222,7 +225,7 @@ def main():
     bcast_ms = 0.0
     if rank == 0:
         x.copy_(spmk.make_dense_device(K, n, DENSE_SEED + n, device=dev))
-    if ws > 1:
+    if use_dist:
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -247,7 +250,7 @@ def main():
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     main_ms = []
     torch.cuda.synchronize()
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = spmk.launch_count()
@@ -263,16 +266,16 @@ def main():
         wall = time.perf_counter() - wall0
     launches = spmk.launch_count() - launches0
     spmk.timing_enable(False)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     dev_ms = sum(e0.elapsed_time(e1) for e0, e1 in ev)
     t_local = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if use_dist:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     t_max_ms = float(t_local.item())
     nnz_all = torch.tensor([a.nnz], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if use_dist:
         dist.all_reduce(nnz_all)
     flops_step = 2.0 * float(nnz_all.item()) * n
     value = flops_step * args.steps / (t_max_ms * 1e-3) / 1e9
@@ -290,7 +293,7 @@ def main():
     for i in range(2):
         a.spmm_host_async(kid, hxn[i], hyn[i], streams[i].cuda_stream)
     torch.cuda.synchronize()
-    if ws > 1:
+    if use_dist:
         dist.barrier()
     flush.zero_()
     torch.cuda.synchronize()
@@ -310,7 +313,7 @@ def main():
         a.spmm_host(kid, hxn[0], stream=stream.cuda_stream, out=hyn[0])
         sync_ms += (time.perf_counter() - t0) * 1e3
     t_e2e = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
+    if use_dist:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_value = flops_step * args.steps / (float(t_e2e.item()) * 1e-3) / 1e9
     ok_e2e = bool(torch.equal(torch.from_numpy(hyn[0].copy()).to(dev), y))
@@ -362,7 +365,7 @@ def main():
     result["clocks"] = clocks
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(a, x, kid, n)
-    if ws > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     if rank == 0:

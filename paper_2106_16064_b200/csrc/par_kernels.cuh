@@ -58,8 +58,6 @@ par_rs_kernel(const ParArgs a) {
   constexpr int V2CT = (CT % 32 == 0) ? 5 : (CT % 16 == 0) ? 4 : (CT % 8 == 0) ? 3 : (CT % 4 == 0) ? 2 : (CT % 2 == 0) ? 1 : 0;
   constexpr int HL = LOGG < V2CT ? LOGG : V2CT;
 
-  // software pipeline over this group's rows: bounds two rows ahead, the
-  // first W-batch of colIdx/val one row ahead, dense rows for the current one
   auto bounds = [&](int row, int& s, int& f) {
     if (row < a.mne) {
       s = a.crp[row];
@@ -113,18 +111,19 @@ par_rs_kernel(const ParArgs a) {
     }
   };
 
-  int s0, f0, s1, f1;
+  // Software pipeline over this group's rows: bounds two rows ahead, the
+  // first W-batch of colIdx/val one row ahead.  Refills happen after the
+  // rotation, so the register moves only read values loaded an iteration
+  // earlier.
+  int s0, f0, s1, f1, s2, f2;
   bounds(gid, s0, f0);
   bounds(gid + groups_total, s1, f1);
-  int c0[VL];
-  float w0[VL];
+  bounds(gid + 2 * groups_total, s2, f2);
+  int c0[VL], c1[VL];
+  float w0[VL], w1[VL];
   first_batch(s0, f0, c0, w0);
+  first_batch(s1, f1, c1, w1);
   for (int r = gid; r < a.mne; r += groups_total) {
-    int s2, f2;
-    bounds(r + 2 * groups_total, s2, f2);
-    int c1[VL];
-    float w1[VL];
-    first_batch(s1, f1, c1, w1);
     const int s = s0, f = f0;
     float acc[CT];
 #pragma unroll
@@ -189,6 +188,8 @@ par_rs_kernel(const ParArgs a) {
       c0[v] = c1[v];
       w0[v] = w1[v];
     }
+    bounds(r + 3 * groups_total, s2, f2);
+    first_batch(s1, f1, c1, w1);
   }
 }
 

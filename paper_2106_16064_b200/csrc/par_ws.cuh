@@ -158,24 +158,28 @@ par_ws_kernel(const ParArgs a) {
   for (int j = 0; j < CT; ++j) carry[j] = 0.f;
 
   // One chunk [c0, c0+W), executed by the whole warp (shuffles full-mask).
+  // Row ends beyond the last window entry read as BIG.  Dead lanes need no
+  // run boundaries of their own: lanes before `lo` belong to row cur, whose
+  // end (= lo) is already a head bit of M; lanes at or past `hi` only follow
+  // live lanes (they never feed a live lane's scan), and the last live lane
+  // is flagged explicitly.  Dead lanes carry w = x = 0.
+  char* const ybase = reinterpret_cast<char*>(a.Y + col0);
+  const long long ystride = (long long)N * 4;
   auto chunk = [&](bool en, int c0, float w, const float (&x)[CT]) {
     const int p = c0 + gl;
     const int hi = min(c0 + W, hard_end);
     const bool live = en && p >= lo && p < hi;
-    const int wi = cur - rbase + gl;
+    const int wbase = cur - rbase;
+    const int wi = wbase + gl;
     const int wend = (en && wi < cnt) ? wcrp[wi] : BIG;
-    const int b = wend - c0;
-    const unsigned M = group_or<W>((b > 0 && b < W) ? (1u << b) : 0u);  // in-chunk row starts
-    unsigned Mrun = M;                                                 // + dead-lane boundaries
-    const int llo = lo - c0, lhi = hi - c0;
-    if (llo > 0 && llo < W) Mrun |= 1u << llo;
-    if (lhi > 0 && lhi < W) Mrun |= 1u << lhi;
-    const unsigned mle = Mrun & le;
+    const unsigned b = (unsigned)(wend - c0);
+    const unsigned M = group_or<W>((b - 1u < (unsigned)(W - 1)) ? (1u << b) : 0u);  // in-chunk row starts
+    const unsigned mle = M & le;
     const int sst = mle ? 31 - __clz(mle) : 0;  // first lane of this lane's run
-    const int kidx = __popc(M & le);            // row(l) - cur
+    const int kidx = __popc(mle);               // row(l) - cur
     float v[CT];
 #pragma unroll
-    for (int j = 0; j < CT; ++j) v[j] = live ? __fmul_rn(w, x[j]) : 0.f;
+    for (int j = 0; j < CT; ++j) v[j] = __fmul_rn(w, x[j]);  // kernels.hpp:277
 #pragma unroll
     for (int off = 1; off < W; off <<= 1) {  // reduction.hpp:77-85, lockstep
       const bool same = gl - off >= sst;
@@ -186,31 +190,29 @@ par_ws_kernel(const ParArgs a) {
       }
     }
     // emission by the last lane of each run
-    const bool last = live && (gl == W - 1 || ((Mrun >> (gl + 1)) & 1u));
+    const bool last = live && (gl == W - 1 || p + 1 == hi || ((M >> (gl + 1)) & 1u));
     const bool first_run = has_carry && kidx == 0;  // run continuing from before c0
-    int rend = 0;
     float t[CT];
 #pragma unroll
     for (int j = 0; j < CT; ++j)
       t[j] = (first_run && mode == MODE_NORMAL) ? __fadd_rn(carry[j], v[j]) : v[j];
+    const int ri = wbase + kidx;
+    const int rend = (last && ri < cnt) ? wcrp[ri] : BIG;
     if (last) {
-      const int ri = cur - rbase + kidx;
-      rend = ri < cnt ? wcrp[ri] : BIG;
-      const bool ends = rend <= c0 + W;
       if (first_run && mode == MODE_ENTER_LONG) {
         store_cols<CT>(a.H + (size_t)(c0 / W) * N + col0, nt, t, false);
-      } else if (ends) {
-        store_cols<CT>(a.Y + (size_t)wrid[ri] * N + col0, nt, t, true);
+      } else if (rend <= c0 + W) {
+        store_cols<CT>(reinterpret_cast<float*>(ybase + (long long)wrid[ri] * ystride), nt, t, true);
       }
     }
     // the last live run continuing past the chunk becomes the carried row
-    const int ll = (lhi >= W ? W : (lhi < 1 ? 1 : lhi)) - 1;
-    const int flags = __shfl_sync(FULL, (rend > c0 + W ? 1 : 0) | (first_run ? 2 : 0), ll, W);
+    const int ll = max(min(hi - c0, W), 1) - 1;
+    const int flags = __shfl_sync(FULL, (rend != BIG && rend > c0 + W ? 1 : 0) | (first_run ? 2 : 0), ll, W);
     float tl[CT];
 #pragma unroll
     for (int j = 0; j < CT; ++j) tl[j] = __shfl_sync(FULL, t[j], ll, W);
     const int nb = __popc(M);
-    const int wn_i = cur - rbase + nb;
+    const int wn_i = wbase + nb;
     const int wn = (en && wn_i < cnt) ? wcrp[wn_i] : BIG;
     if (en) {
       if (flags & 1) {

@@ -242,18 +242,20 @@ seq_kernel(const SeqArgs a) {
     }
   };
 
+  // colIdx/val two batches ahead (refilled after the rotation, so the moves
+  // read registers loaded an iteration earlier); dense rows one batch ahead in
+  // two register sets whose roles swap between the two unrolled halves.
   int c_c[SLOTS], c_n[SLOTS], c_nn[SLOTS];
   float v_c[SLOTS], v_n[SLOTS], v_nn[SLOTS];
-  float x_c[B][CPL], x_n[B][CPL];
+  float x_a[B][CPL], x_b[B][CPL];
   load_cv(st.e, c_c, v_c);
   load_cv(st.e + B, c_n, v_n);
+  load_cv(st.e + 2 * B, c_nn, v_nn);
   st.setup_end(a);
-  load_x(st.e, c_c, x_c);
+  load_x(st.e, c_c, x_a);
 
-#pragma unroll 1
-  for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += B) {
-    load_cv(eb + 2 * B, c_nn, v_nn);
-    load_x(eb + B, c_n, x_n);
+  auto step = [&](int eb, float (&xc)[B][CPL], float (&xn)[B][CPL]) {
+    load_x(eb + B, c_n, xn);
     float vv[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) vv[j] = gshfl<LPU>(v_c[j / LPU], j % LPU);
@@ -269,24 +271,27 @@ seq_kernel(const SeqArgs a) {
       for (int j = 0; j < B; ++j) {
         if (j >= js && j < je) {
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) st.acc[k] = mul_add_rn(st.acc[k], vv[j], x_c[j][k]);
+          for (int k = 0; k < CPL; ++k) st.acc[k] = mul_add_rn(st.acc[k], vv[j], xc[j][k]);
         }
       }
       if (je >= B) break;
       st.event(a, eb + je);
       js = je;
     }
-    // rotate the pipeline
-#pragma unroll
-    for (int j = 0; j < B; ++j)
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) x_c[j][k] = x_n[j][k];
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
       v_c[s] = v_n[s];
       c_n[s] = c_nn[s];
       v_n[s] = v_nn[s];
     }
+    load_cv(eb + 3 * B, c_nn, v_nn);
+  };
+
+#pragma unroll 1
+  for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += 2 * B) {
+    step(eb, x_a, x_b);
+    if (!__any_sync(0xffffffffu, st.live)) break;
+    step(eb + B, x_b, x_a);
   }
 }
 
@@ -365,7 +370,7 @@ seq_kernel_async(const SeqArgs a) {
   int cring[R][SLOTS];
   float vring[R][SLOTS];
 #pragma unroll
-  for (int r = 0; r < R - 1; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
+  for (int r = 0; r < R; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
   st.setup_end(a);
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(st.e + s * B, s, cring[s]);
@@ -373,7 +378,6 @@ seq_kernel_async(const SeqArgs a) {
   int stage = 0;
 #pragma unroll 1
   for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += B) {
-    load_cv(eb + (R - 1) * B, cring[R - 1], vring[R - 1]);
     issue(eb + (S - 1) * B, (stage + S - 1) % S, cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     // products of the whole batch up front (smem latency off the add chain);
@@ -408,6 +412,8 @@ seq_kernel_async(const SeqArgs a) {
       js = ev ? je : B;
     }
     stage = (stage + 1 == S) ? 0 : stage + 1;
+    // rotate, then refill the top slot R batches ahead: the moves only read
+    // registers loaded an iteration earlier (no wait on this iteration's loads)
 #pragma unroll
     for (int r = 0; r + 1 < R; ++r)
 #pragma unroll
@@ -415,6 +421,7 @@ seq_kernel_async(const SeqArgs a) {
         cring[r][s] = cring[r + 1][s];
         vring[r][s] = vring[r + 1][s];
       }
+    load_cv(eb + R * B, cring[R - 1], vring[R - 1]);
   }
   cp_async_wait<0>();
 }
@@ -610,7 +617,7 @@ seq_async2_kernel(const SeqArgs a) {
   int cring[S + 1][SLOTS];
   float vring[S + 1][SLOTS];
 #pragma unroll
-  for (int i = 0; i < S; ++i) load_cv(ea + i * B, cring[i], vring[i]);
+  for (int i = 0; i <= S; ++i) load_cv(ea + i * B, cring[i], vring[i]);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
     if (ea + s * LPU + st.gl < st.e) vring[0][s] = 0.f;  // other rows before the unit start
@@ -621,7 +628,6 @@ seq_async2_kernel(const SeqArgs a) {
   int stage = 0;
 #pragma unroll 1
   for (int eb = ea; __any_sync(FULL, st.live); eb += B) {
-    load_cv(eb + S * B, cring[S], vring[S]);
     issue((stage + S - 1) & (S - 1), cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     const float4* xs = ring + stage * B * NT + threadIdx.x;
@@ -666,6 +672,9 @@ seq_async2_kernel(const SeqArgs a) {
       js = je;
     }
     stage = (stage + 1) & (S - 1);
+    // Rotate the colIdx/val ring, then load the batch S+1 ahead into the top
+    // slot: the moves read registers loaded one full iteration earlier, so
+    // they never wait on a load issued in this iteration.
 #pragma unroll
     for (int i = 0; i < S; ++i)
 #pragma unroll
@@ -673,6 +682,7 @@ seq_async2_kernel(const SeqArgs a) {
         cring[i][s] = cring[i + 1][s];
         vring[i][s] = vring[i + 1][s];
       }
+    load_cv(eb + (S + 1) * B, cring[S], vring[S]);
   }
   cp_async_wait<0>();
 }
