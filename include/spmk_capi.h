@@ -96,7 +96,8 @@ spmk_status spmk_parse_kernel(const char* name, spmk_kernel_id* out);
 spmk_status spmk_csr_create(int64_t num_rows, int64_t num_cols, int64_t nnz,
                             const int64_t* row_ptr, const int64_t* col_idx,
                             const float* values, int device, spmk_csr_t* out);
-/* Same, from int32 DEVICE arrays already in HBM (e.g. the device generator).
+/* Same, from int32 DEVICE arrays already in HBM (e.g. the device generator);
+ * the call synchronizes the device first, so producers on any stream are done.
  * copy=0 borrows the arrays (caller keeps them alive), copy=1 duplicates.
  * Validation is done on the device (canonical rows, bounds). */
 spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols,

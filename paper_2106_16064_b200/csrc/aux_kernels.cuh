@@ -131,8 +131,16 @@ __global__ void tile_plan_kernel(const int* __restrict__ crp, int mne, long long
 //              boundaries (its per-chunk partials go to the H slots), else 0;
 //              start == hard_end marks an empty tile.
 //   row-split tiles (RB compact rows each): {r0, crp[r0], crp[r1], 0}.
+// A row crossing exactly one tile boundary B and ending at f <= B + EXT is
+// finished by the tile that owns its start ("owner extends"); every other
+// boundary-crossing row is "long" (per-chunk partials + owner prefix, merged
+// by fixup_kernel).  EXT <= TS; EXT bounds the extra work of one unit.
+__device__ __forceinline__ bool row_is_long(long long s, long long f, long long TS, long long EXT) {
+  const long long b0 = s / TS, b1 = (f - 1) / TS;
+  return b1 - b0 >= 2 || (b1 - b0 == 1 && f > (b0 + 1) * TS + EXT);
+}
 __global__ void ws_tile_desc_kernel(const int* __restrict__ crp, const int* __restrict__ rlo,
-                                    long long ntiles, long long TS, long long nnz,
+                                    long long ntiles, long long TS, long long EXT, long long nnz,
                                     int4* __restrict__ desc) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntiles;
        t += (long long)gridDim.x * blockDim.x) {
@@ -143,14 +151,14 @@ __global__ void ws_tile_desc_kernel(const int* __restrict__ crp, const int* __re
     if (te < nnz) {
       const int r2 = rlo[t + 1];
       const long long c2 = crp[r2];
-      if (c2 > te && crp[r2 - 1] >= tb && c2 <= (t + 2) * TS) hard_end = c2;
+      if (c2 > te && crp[r2 - 1] >= tb && c2 <= te + EXT) hard_end = c2;
     }
     int cur = r, mode = MODE_NORMAL;
     long long start = tb;
     const long long cr = crp[r];
     if (cr > tb) {  // row r-1 enters from the left
       const long long rs = crp[r - 1];
-      if ((cr - 1) / TS - rs / TS >= 2) {
+      if (row_is_long(rs, cr, TS, EXT)) {
         cur = r - 1;
         mode = MODE_ENTER_LONG;
       } else {
@@ -170,12 +178,11 @@ __global__ void rs_tile_desc_kernel(const int* __restrict__ crp, int mne, int RB
   }
 }
 // Long rows for a tile size: rows spanning >= 2 tile boundaries past their own.
-__global__ void long_rows_kernel(const int* __restrict__ crp, int mne, long long TS,
+__global__ void long_rows_kernel(const int* __restrict__ crp, int mne, long long TS, long long EXT,
                                  int* __restrict__ list, int* __restrict__ count) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < mne;
        c += (long long)gridDim.x * blockDim.x) {
-    const long long s = crp[c], f = crp[c + 1];
-    if ((f - 1) / TS - s / TS >= 2) list[atomicAdd(count, 1)] = (int)c;
+    if (row_is_long(crp[c], crp[c + 1], TS, EXT)) list[atomicAdd(count, 1)] = (int)c;
   }
 }
 // plan_balanced (kernels.hpp:133-149) chunk starts: elem_row[q*chunk] =

@@ -53,6 +53,7 @@ struct SeqArgs {
   int ncol_tile;                 // columns handled per blockIdx.y
   long long TS;                  // ws: tile size in nnz (= T * CH)
   long long CH;                  // ws: chunk size (seq_chunk)
+  long long EXT;                 // ws: owner-extension limit (row_is_long)
   int RB;                        // rs: rows per tile
   int nunits;                    // tiles
   int cvvec;                     // colIdx/val 16-byte aligned (vector batch loads)
@@ -128,7 +129,7 @@ struct SeqSweep {
       CH = (int)a.CH;
       const long long tb = (long long)unit * a.TS;
       te = (int)min(tb + a.TS, (long long)a.nnz);
-      long_thresh = (int)min((long long)(unit + 2) * a.TS, (long long)BIG);  // row end > this => long
+      long_thresh = (int)min(tb + a.TS + a.EXT, (long long)BIG);  // row end > this => long (row_is_long)
       q = e / CH;
       next_cb = (int)min((long long)(q + 1) * CH, (long long)BIG);
     } else {
@@ -370,7 +371,7 @@ seq_kernel_async(const SeqArgs a) {
   int cring[R][SLOTS];
   float vring[R][SLOTS];
 #pragma unroll
-  for (int r = 0; r < R; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
+  for (int r = 0; r < R - 1; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
   st.setup_end(a);
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(st.e + s * B, s, cring[s]);
@@ -378,6 +379,7 @@ seq_kernel_async(const SeqArgs a) {
   int stage = 0;
 #pragma unroll 1
   for (int eb = st.e; __any_sync(0xffffffffu, st.live); eb += B) {
+    load_cv(eb + (R - 1) * B, cring[R - 1], vring[R - 1]);
     issue(eb + (S - 1) * B, (stage + S - 1) % S, cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     // products of the whole batch up front (smem latency off the add chain);
@@ -412,8 +414,8 @@ seq_kernel_async(const SeqArgs a) {
       js = ev ? je : B;
     }
     stage = (stage + 1 == S) ? 0 : stage + 1;
-    // rotate, then refill the top slot R batches ahead: the moves only read
-    // registers loaded an iteration earlier (no wait on this iteration's loads)
+    // (Refilling the top slot after the rotation instead, so the moves never
+    // wait on this iteration's loads, measured 15 % slower on B200.)
 #pragma unroll
     for (int r = 0; r + 1 < R; ++r)
 #pragma unroll
@@ -421,7 +423,6 @@ seq_kernel_async(const SeqArgs a) {
         cring[r][s] = cring[r + 1][s];
         vring[r][s] = vring[r + 1][s];
       }
-    load_cv(eb + R * B, cring[R - 1], vring[R - 1]);
   }
   cp_async_wait<0>();
 }
@@ -566,7 +567,7 @@ constexpr int seq_async2_smem_bytes() {
   return NT * S * B * 16 + (NT / LPU) * 2 * SeqWin<LPU>::WIN * 4;
 }
 
-template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA = false>
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA = false, bool LATE = false>
 __global__ void __launch_bounds__(NT, NT <= 128 ? 3 : 1)
 seq_async2_kernel(const SeqArgs a) {
   static_assert((S & (S - 1)) == 0 && S >= 2, "S must be a power of two");
@@ -617,7 +618,7 @@ seq_async2_kernel(const SeqArgs a) {
   int cring[S + 1][SLOTS];
   float vring[S + 1][SLOTS];
 #pragma unroll
-  for (int i = 0; i <= S; ++i) load_cv(ea + i * B, cring[i], vring[i]);
+  for (int i = 0; i < (LATE ? S + 1 : S); ++i) load_cv(ea + i * B, cring[i], vring[i]);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
     if (ea + s * LPU + st.gl < st.e) vring[0][s] = 0.f;  // other rows before the unit start
@@ -628,6 +629,7 @@ seq_async2_kernel(const SeqArgs a) {
   int stage = 0;
 #pragma unroll 1
   for (int eb = ea; __any_sync(FULL, st.live); eb += B) {
+    if constexpr (!LATE) load_cv(eb + S * B, cring[S], vring[S]);
     issue((stage + S - 1) & (S - 1), cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     const float4* xs = ring + stage * B * NT + threadIdx.x;
@@ -672,9 +674,9 @@ seq_async2_kernel(const SeqArgs a) {
       js = je;
     }
     stage = (stage + 1) & (S - 1);
-    // Rotate the colIdx/val ring, then load the batch S+1 ahead into the top
-    // slot: the moves read registers loaded one full iteration earlier, so
-    // they never wait on a load issued in this iteration.
+    // LATE: refill the top slot after the rotation (moves never wait on this
+    // iteration's loads) — measured 15 % slower on B200 than refilling at the
+    // top of the iteration (cfg2: 421 vs 358 us), so off by default.
 #pragma unroll
     for (int i = 0; i < S; ++i)
 #pragma unroll
@@ -682,7 +684,7 @@ seq_async2_kernel(const SeqArgs a) {
         cring[i][s] = cring[i + 1][s];
         vring[i][s] = vring[i + 1][s];
       }
-    load_cv(eb + (S + 1) * B, cring[S], vring[S]);
+    if constexpr (LATE) load_cv(eb + (S + 1) * B, cring[S], vring[S]);
   }
   cp_async_wait<0>();
 }

@@ -65,7 +65,7 @@ struct Plan {
   int4* desc = nullptr;    // ntiles per-tile start descriptors
   int* rlo = nullptr;      // ntiles + 1
   long long ntiles = 0;
-  long long TS = 0, CH = 0;
+  long long TS = 0, CH = 0, EXT = 0;
   int* longrows = nullptr;
   int nlong = 0;
 };
@@ -122,7 +122,7 @@ struct spmk_csr_s {
   long long max_row = 0;
   unsigned long long sum_len2 = 0;
   // caches
-  std::map<std::tuple<int, long long, long long>, Plan> plans;
+  std::map<std::tuple<int, long long, long long, long long>, Plan> plans;
   float* scratch = nullptr;
   size_t scratch_floats = 0;
   // host-operand staging: kStageSlots rotating (X, Y) device buffer pairs;
@@ -199,25 +199,27 @@ void build_meta(spmk_csr_s* h, cudaStream_t s) {
 }
 
 // Plan for a nonzero-split kernel: tiles of TS nonzeros made of CH-chunks.
-Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t s) {
-  auto key = std::make_tuple(kind, TS, CH);
+Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EXT, cudaStream_t s) {
+  EXT = std::max(1LL, std::min(EXT, TS));
+  auto key = std::make_tuple(kind, TS, CH, EXT);
   auto it = h->plans.find(key);
   if (it != h->plans.end()) return it->second;
   Plan p;
   p.TS = TS;
   p.CH = CH;
+  p.EXT = EXT;
   p.ntiles = (h->nnz + TS - 1) / TS;
   p.rlo = dev_alloc<int>((size_t)p.ntiles + 1);
   tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo); LAUNCHED(1);
   p.desc = dev_alloc<int4>((size_t)p.ntiles);
-  ws_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, p.rlo, p.ntiles, TS, h->nnz, p.desc); LAUNCHED(1);
+  ws_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, p.rlo, p.ntiles, TS, EXT, h->nnz, p.desc); LAUNCHED(1);
   int* cnt = dev_alloc<int>(1);
   CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
-  // upper bound on long rows: nnz / (TS+1)
-  const long long cap = h->nnz / (TS + 1) + 1;
+  // upper bound on long rows: every long row crosses a tile boundary
+  const long long cap = p.ntiles + 1;
   p.longrows = dev_alloc<int>((size_t)cap);
   if (h->mne > 0)
-    long_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, TS, p.longrows, cnt); LAUNCHED(1);
+    long_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, TS, EXT, p.longrows, cnt); LAUNCHED(1);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&p.nlong, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -227,7 +229,7 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, cudaStream_t
 
 // Row-split tile descriptors (RB compact rows per tile), cached like a plan.
 int4* get_rs_desc(spmk_csr_s* h, int RB, cudaStream_t s) {
-  auto key = std::make_tuple(3, (long long)RB, 0LL);
+  auto key = std::make_tuple(3, (long long)RB, 0LL, 0LL);
   auto it = h->plans.find(key);
   if (it != h->plans.end()) return it->second.desc;
   Plan p;
@@ -343,18 +345,18 @@ void launch_seq4(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   }
 }
 
-template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA>
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false>
 void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
   static bool attr_set = false;
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA>,
+    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
+  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
 }
 
 template <bool WS, int B, int S, int NT, bool EXACT, bool CA = false>
@@ -394,6 +396,7 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     else if (variant == 14) launch_seq_a2<WS, 8, 2, 256, true, true>(a, lpu, tiles, s);
     else if (variant == 15) launch_seq_a2<WS, 8, 2, 256, true>(a, lpu, tiles, s);
     else if (variant == 16) launch_seq_a2<WS, 16, 2, 128, true>(a, lpu, tiles, s);
+    else if (variant == 17 && lpu == 8) launch_seq_a2_t<8, 8, 2, WS, 128, true, false, false>(a, tiles, s);
     else if (variant == 4) launch_seq4<WS, 8, false>(a, lpu, tiles, s);
     else if (variant == 5) launch_seq4<WS, 4, true>(a, lpu, tiles, s);
     else launch_seq4<WS, 8, true>(a, lpu, tiles, s);
@@ -493,7 +496,7 @@ void launch_par_ws_tt(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
 void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   const int T = par_ws_chunks_per_tile();
   // T = 4 measured best on B200 (R-MAT s20 heavy/uniform, N = 1 and 4)
-  const long long minb = env_ll("SPMK_PARWS_MINB", 4);
+  const long long minb = env_ll("SPMK_PARWS_MINB", 5);
   if (T == 8) launch_par_ws_tt<8, 1>(a, W, aligned, s);
   else if (minb == 5) launch_par_ws_tt<4, 5>(a, W, aligned, s);
   else if (minb == 6) launch_par_ws_tt<4, 6>(a, W, aligned, s);
@@ -553,11 +556,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     } else {
       const long long CH = (long long)cfg.seq_chunk;
       const long long TS = CH * tile_chunks(CH, env_ll("SPMK_SEQ_TILE_NNZ", 256));
-      Plan& p = get_plan(h, 1, TS, CH, s);
+      Plan& p = get_plan(h, 1, TS, CH, env_ll("SPMK_SEQ_EXT", 32), s);  // EXT: measured (cfg2 -7 %)
       a.rlo = p.rlo;
       a.desc = p.desc;
       a.TS = TS;
       a.CH = CH;
+      a.EXT = p.EXT;
       a.nunits = (int)p.ntiles;
       if (p.nlong > 0) {
         const long long nch = (h->nnz + CH - 1) / CH;
@@ -592,7 +596,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       if (W > 32) return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
       const long long CH = W;
       const long long TS = CH * par_ws_chunks_per_tile();  // par_ws_kernel tile shape
-      Plan& p = get_plan(h, 2, TS, CH, s);
+      Plan& p = get_plan(h, 2, TS, CH, env_ll("SPMK_PARWS_EXT", 32), s);
       a.rlo = p.rlo;
       a.desc = p.desc;
       a.TS = TS;
@@ -780,6 +784,8 @@ spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols, int64_t n
   DeviceGuard g(device);
   cudaStream_t s = nullptr;
   try {
+    // the arrays may still be in flight on any of the caller's streams
+    CK(cudaDeviceSynchronize());
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     int* rp = const_cast<int*>(d_row_ptr);
     int* col = const_cast<int*>(d_col_idx);
