@@ -87,7 +87,7 @@ __device__ __forceinline__ void store_cols(float* __restrict__ p, int nt, const 
     }
 }
 
-template <int W, int CT, int T = kParWsChunksPerTile, int MINB = 1>
+template <int W, int CT, int T = kParWsChunksPerTile, int MINB = 1, bool BATCHED = true>
 __global__ void __launch_bounds__(256, MINB)
 par_ws_kernel(const ParArgs a) {
   static_assert(W >= 2 && W <= 32, "W");
@@ -233,10 +233,106 @@ par_ws_kernel(const ParArgs a) {
     }
   };
 
+  if constexpr (!BATCHED) {
 #pragma unroll
-  for (int k = 0; k < T; ++k) {
-    const int c0 = tb + k * W;
-    chunk(work && c0 < te && c0 + W > lo, c0, wv[k], xv[k]);
+    for (int k = 0; k < T; ++k) {
+      const int c0 = tb + k * W;
+      chunk(work && c0 < te && c0 + W > lo, c0, wv[k], xv[k]);
+    }
+  } else {
+    // Batched form: the segment heads of the whole tile are known up front
+    // (one bitmap word per chunk: bit e-tb for every row end e inside the
+    // tile), so the T conditional scans are independent straight-line code
+    // the scheduler interleaves; only the (cheap) emission/carry pass below
+    // is sequential over the chunks.
+    unsigned hw[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) hw[k] = 0u;
+    for (int i = gl; i < cnt; i += W) {
+      const int off = wcrp[i] - tb;
+      if (off > 0 && off < T * W) {
+#pragma unroll
+        for (int k = 0; k < T; ++k)
+          if ((off / W) == k) hw[k] |= 1u << (off % W);
+      }
+    }
+    unsigned M[T];
+    int base[T + 1];
+    base[0] = 0;
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      M[k] = group_or<W>(hw[k]);
+      base[k + 1] = base[k] + __popc(M[k]);
+    }
+    float v[T][CT];
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+#pragma unroll
+      for (int j = 0; j < CT; ++j) v[k][j] = __fmul_rn(wv[k], xv[k][j]);  // kernels.hpp:277
+    int sst[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const unsigned mle = M[k] & le;
+      sst[k] = mle ? 31 - __clz(mle) : 0;
+    }
+#pragma unroll
+    for (int off = 1; off < W; off <<= 1) {  // reduction.hpp:77-85, lockstep, T chunks interleaved
+#pragma unroll
+      for (int k = 0; k < T; ++k) {
+        const bool same = gl - off >= sst[k];
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          const float up = __shfl_up_sync(FULL, v[k][j], off, W);
+          if (same) v[k][j] = __fadd_rn(v[k][j], up);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      const int c0 = tb + k * W;
+      const bool en = work && c0 < te && c0 + W > lo;
+      const int p = c0 + gl;
+      const int hi = min(c0 + W, hard_end);
+      const bool live = en && p >= lo && p < hi;
+      const int kl = __popc(M[k] & le);
+      const bool last = live && (gl == W - 1 || p + 1 == hi || ((M[k] >> (gl + 1)) & 1u));
+      const bool first_run = has_carry && kl == 0;  // run continuing from before c0
+      float t[CT];
+#pragma unroll
+      for (int j = 0; j < CT; ++j)
+        t[j] = (first_run && mode == MODE_NORMAL) ? __fadd_rn(carry[j], v[k][j]) : v[k][j];
+      const int ri = base[k] + kl;  // window index of this lane's row
+      const int rend = (last && ri < cnt) ? wcrp[ri] : BIG;
+      if (last) {
+        if (first_run && mode == MODE_ENTER_LONG) {
+          store_cols<CT>(a.H + (size_t)(c0 / W) * N + col0, nt, t, false);
+        } else if (rend <= c0 + W) {
+          store_cols<CT>(reinterpret_cast<float*>(ybase + (long long)wrid[ri] * ystride), nt, t, true);
+        }
+      }
+      const int ll = max(min(hi - c0, W), 1) - 1;
+      const int flags = __shfl_sync(FULL, (rend != BIG && rend > c0 + W ? 1 : 0) | (first_run ? 2 : 0), ll, W);
+      float tl[CT];
+#pragma unroll
+      for (int j = 0; j < CT; ++j) tl[j] = __shfl_sync(FULL, t[j], ll, W);
+      if (en) {
+        if (flags & 1) {
+          if (!(flags & 2)) {
+#pragma unroll
+            for (int j = 0; j < CT; ++j) carry[j] = __fadd_rn(0.f, tl[j]);  // Y starts at +0
+            has_carry = true;
+            mode = MODE_NORMAL;
+          } else if (mode == MODE_NORMAL) {
+#pragma unroll
+            for (int j = 0; j < CT; ++j) carry[j] = tl[j];
+          }
+        } else {
+          has_carry = false;
+          mode = MODE_NORMAL;
+        }
+      }
+    }
+    cur = rbase + base[T];  // row containing te (the extension row, if any)
   }
   // long row crossing te (its owner does not extend): prefix -> T slot
   if (work && hard_end == te && has_carry && mode == MODE_NORMAL && gl == 0)

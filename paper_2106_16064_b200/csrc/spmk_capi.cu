@@ -133,6 +133,9 @@ struct spmk_csr_s {
   size_t stage_x_n[kStageSlots] = {0, 0}, stage_y_n[kStageSlots] = {0, 0};
   cudaEvent_t slot_done[kStageSlots] = {nullptr, nullptr};
   int next_slot = 0;
+  // side stream for work that overlaps the variant kernels (empty-row fill)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
 };
 
@@ -152,6 +155,12 @@ void free_handle(spmk_csr_s* h) {
     cudaFree(kv.second.longrows);
   }
   cudaFree(h->scratch);
+  if (h->side) {
+    cudaStreamSynchronize(h->side);
+    cudaStreamDestroy(h->side);
+    cudaEventDestroy(h->ev_fork);
+    cudaEventDestroy(h->ev_join);
+  }
   for (int i = 0; i < spmk_csr_s::kStageSlots; ++i) {
     cudaFree(h->stage_x[i]);
     cudaFree(h->stage_y[i]);
@@ -456,14 +465,14 @@ void launch_par_rs(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   }
 }
 
-template <int W, int CT, int T, int MINB>
+template <int W, int CT, int T, int MINB, bool BT>
 void launch_par_ws_t(const ParArgs& a, int ncol_tiles, cudaStream_t s) {
   const int upb = 256 / W;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  par_ws_kernel<W, CT, T, MINB><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
+  par_ws_kernel<W, CT, T, MINB, BT><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
 }
 
-template <int W, int T, int MINB>
+template <int W, int T, int MINB, bool BT>
 void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
   const int N = a.N;
   int ct = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : 8;
@@ -471,10 +480,10 @@ void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
   a.ncol_tile = ct;
   const int tiles = (N + ct - 1) / ct;
   switch (ct) {
-    case 1: launch_par_ws_t<W, 1, T, MINB>(a, tiles, s); break;
-    case 2: launch_par_ws_t<W, 2, T, MINB>(a, tiles, s); break;
-    case 4: launch_par_ws_t<W, 4, T, MINB>(a, tiles, s); break;
-    default: launch_par_ws_t<W, 8, T, MINB>(a, tiles, s); break;
+    case 1: launch_par_ws_t<W, 1, T, MINB, BT>(a, tiles, s); break;
+    case 2: launch_par_ws_t<W, 2, T, MINB, BT>(a, tiles, s); break;
+    case 4: launch_par_ws_t<W, 4, T, MINB, BT>(a, tiles, s); break;
+    default: launch_par_ws_t<W, 8, T, MINB, BT>(a, tiles, s); break;
   }
 }
 
@@ -482,14 +491,14 @@ void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
 // knob: any T keeps the results bit-exact).
 int par_ws_chunks_per_tile() { return (int)env_ll("SPMK_PARWS_T", 4); }
 
-template <int T, int MINB>
+template <int T, int MINB, bool BT = true>
 void launch_par_ws_tt(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   switch (W) {
-    case 2: launch_par_ws_w<2, T, MINB>(a, aligned, s); break;
-    case 4: launch_par_ws_w<4, T, MINB>(a, aligned, s); break;
-    case 8: launch_par_ws_w<8, T, MINB>(a, aligned, s); break;
-    case 16: launch_par_ws_w<16, T, MINB>(a, aligned, s); break;
-    default: launch_par_ws_w<32, T, MINB>(a, aligned, s); break;
+    case 2: launch_par_ws_w<2, T, MINB, BT>(a, aligned, s); break;
+    case 4: launch_par_ws_w<4, T, MINB, BT>(a, aligned, s); break;
+    case 8: launch_par_ws_w<8, T, MINB, BT>(a, aligned, s); break;
+    case 16: launch_par_ws_w<16, T, MINB, BT>(a, aligned, s); break;
+    default: launch_par_ws_w<32, T, MINB, BT>(a, aligned, s); break;
   }
 }
 
@@ -498,6 +507,7 @@ void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   // T = 4 measured best on B200 (R-MAT s20 heavy/uniform, N = 1 and 4)
   const long long minb = env_ll("SPMK_PARWS_MINB", 5);
   if (T == 8) launch_par_ws_tt<8, 1>(a, W, aligned, s);
+  else if (env_ll("SPMK_PARWS_V", 2) == 1) launch_par_ws_tt<4, 5, false>(a, W, aligned, s);
   else if (minb == 5) launch_par_ws_tt<4, 5>(a, W, aligned, s);
   else if (minb == 6) launch_par_ws_tt<4, 6>(a, W, aligned, s);
   else launch_par_ws_tt<4, 4>(a, W, aligned, s);
@@ -520,16 +530,30 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     return SPMK_OK;
   }
   if (n > INT32_MAX / 2) return fail(SPMK_EUNSUPPORTED, "n too large");
+  if (id == SPMK_PAR_BALANCED && cfg.lane_width > 32)
+    return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
   timing_record(0, s);
   const int N = (int)n;
   const bool aligned = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
-  // empty rows -> 0 (the reference's zero-initialised Y)
-  if (h->nempty > 0) {
-    if (aligned && N % 4 == 0) {
-      zero_rows_kernel<4><<<grid_for((long long)h->nempty * N / 4), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
-    } else {
-      zero_rows_kernel<1><<<grid_for((long long)h->nempty * N), 256, 0, s>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+  // Empty rows -> 0 (the reference's zero-initialised Y).  The variant
+  // kernels never touch empty rows, so the zero fill runs on the handle's
+  // side stream concurrently with them (fork/join through events: HBM writes
+  // overlap the gather-bound sweep; capturable into CUDA graphs).
+  const bool fork = h->nempty > 0;
+  if (fork) {
+    if (!h->side) {
+      CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
     }
+    CK(cudaEventRecord(h->ev_fork, s));
+    CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    if (aligned && N % 4 == 0) {
+      zero_rows_kernel<4><<<grid_for((long long)h->nempty * N / 4), 256, 0, h->side>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+    } else {
+      zero_rows_kernel<1><<<grid_for((long long)h->nempty * N), 256, 0, h->side>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
+    }
+    CK(cudaEventRecord(h->ev_join, h->side));
   }
 
   if (id == SPMK_SEQ_ROWSPLIT || id == SPMK_SEQ_BALANCED) {
@@ -593,7 +617,6 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_rs(a, W, aligned, s);
       timing_record(2, s);
     } else {
-      if (W > 32) return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
       const long long CH = W;
       const long long TS = CH * par_ws_chunks_per_tile();  // par_ws_kernel tile shape
       Plan& p = get_plan(h, 2, TS, CH, env_ll("SPMK_PARWS_EXT", 32), s);
@@ -615,6 +638,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
             p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
     }
   }
+  if (fork) CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   CK(cudaGetLastError());
   timing_record(3, s);
   return SPMK_OK;
