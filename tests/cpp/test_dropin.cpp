@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -160,6 +161,67 @@ TEST_CASE("validate rejects malformed CSR (test_core.cpp:177-191)", false) {
   auto b = two_by_two();
   b.row_ptr.back() = 5;
   CHECK_THROWS_AS(validate(b), Error);
+}
+
+TEST_CASE("matrix market: general, symmetric, pattern, integer (test_io.cpp:11-103)", false) {
+  std::istringstream g("%%MatrixMarket matrix coordinate real general\n% a comment\n\n2 2 2\n1 1 1.0\n2 2 4.0\n");
+  auto a = read_matrix_market<float>(g);
+  CHECK(a.num_rows == 2 && a.num_cols == 2);
+  CHECK(a.row_ptr == (std::vector<Index>{0, 1, 2}));
+  CHECK(a.col_idx == (std::vector<Index>{0, 1}));
+  CHECK(a.values == (std::vector<float>{1.f, 4.f}));
+  std::istringstream sy("%%MatrixMarket matrix coordinate real symmetric\n3 3 3\n2 1 5.0\n3 3 1.0\n3 1 2.0\n");
+  auto coo = read_matrix_market<float>(sy).to_coo();
+  CHECK(coo.size() == 5u);
+  CHECK(coo[0].row == 0 && coo[0].col == 1 && coo[0].value == 5.f);
+  CHECK(coo[1].col == 2 && coo[1].value == 2.f);
+  CHECK(coo[2].row == 1 && coo[2].col == 0);
+  std::istringstream pat("%%MatrixMarket matrix coordinate pattern general\n2 3 2\n1 3\n2 1\n");
+  auto p = read_matrix_market<float>(pat);
+  CHECK(p.values == (std::vector<float>{1.f, 1.f}));
+  std::istringstream in("%%MatrixMarket matrix coordinate integer general\n1 1 1\n1 1 7\n");
+  CHECK(read_matrix_market<float>(in).values == (std::vector<float>{7.f}));
+}
+
+TEST_CASE("matrix market: rejected headers and located errors (test_io.cpp:104-150)", false) {
+  for (const char* h : {"%%MatrixMarket matrix coordinate complex general",
+                        "%%MatrixMarket matrix coordinate real skew-symmetric",
+                        "%%MatrixMarket matrix coordinate real hermitian", "%%MatrixMarket matrix array real general",
+                        "%%MatrixMarket vector coordinate real general", "MatrixMarket matrix coordinate real general"}) {
+    std::istringstream in(std::string(h) + "\n1 1 0\n");
+    CHECK_THROWS_AS(read_matrix_market<float>(in), Error);
+  }
+  auto message_of = [](const std::string& text) {
+    std::istringstream in(text);
+    try {
+      read_matrix_market<float>(in);
+    } catch (const Error& e) {
+      return std::string(e.what());
+    }
+    return std::string();
+  };
+  const std::string m1 = message_of("%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n");
+  CHECK(m1.find("line 3") != std::string::npos && m1.find("bounds") != std::string::npos);
+  CHECK(message_of("%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n").find("truncated") !=
+        std::string::npos);
+  CHECK(!message_of("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 oops 1.0\n").empty());
+}
+
+TEST_CASE("matrix market: writer format and round trip (test_io.cpp:152-198)", false) {
+  auto a = csr_from_coo<float>({{0, 0, 1.f}, {1, 1, 4.f}}, 2, 2);
+  std::ostringstream out;
+  write_matrix_market(a, out);
+  CHECK(out.str() == "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n2 2 4\n");
+  std::ostringstream e;
+  write_matrix_market(csr_from_coo<float>({}, 3, 3), e);
+  CHECK(e.str() == "%%MatrixMarket matrix coordinate real general\n3 3 0\n");
+  std::vector<Triple<float>> t;
+  for (Index i = 0; i < 50; ++i)
+    for (Index j = 0; j < 50; j += 1 + (i % 7)) t.push_back({i, j, 1.0f / float(1 + i + j)});
+  auto b = csr_from_coo(std::move(t), 50, 50);
+  std::stringstream buf;
+  write_matrix_market(b, buf);
+  CHECK(read_matrix_market<float>(buf) == b);
 }
 
 // ------------------------------------------------------------- device path
