@@ -79,7 +79,8 @@ par_rs_kernel(const ParArgs a) {
 #pragma unroll
     for (int v = 0; v < VL; ++v) {
       if (c[v] >= 0) {
-        const float* xr = a.X + (size_t)c[v] * N + col0;
+        const float* xr = reinterpret_cast<const float*>(
+            reinterpret_cast<const char*>(a.X + col0) + (size_t)(unsigned)c[v] * ((unsigned)N * 4u));
         float xv[CT];
         if constexpr (VEC4 && CT % 4 == 0) {
 #pragma unroll

@@ -112,6 +112,10 @@ par_ws_kernel(const ParArgs a) {
   const bool vec = a.xvec != 0;
   const uint64_t pol = evict_first_policy();
   const unsigned le = (gl == 31) ? FULL : ((2u << gl) - 1u);  // lanes <= gl
+  // dense-row address = xb + col * xs: one IMAD.WIDE.U32 per gather
+  const char* const xb = reinterpret_cast<const char*>(a.X + col0);
+  const unsigned xs = (unsigned)N * 4u;
+  auto xrow = [&](int c) { return reinterpret_cast<const float*>(xb + (size_t)(unsigned)c * xs); };
 
   // ---- tile setup from the precomputed descriptor {cur, start, hard_end, mode}
   const int TS = (int)a.TS;
@@ -133,23 +137,30 @@ par_ws_kernel(const ParArgs a) {
   // ---- issue every load of the tile: colIdx/val, then the row window, then X
   int cidx[T];
   float wv[T];
+  const int* const colp = a.col + (tb + gl);  // chunk k at immediate offset k*W
+  const float* const valp = a.val + (tb + gl);
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int p = tb + k * W + gl;
     const bool live = work && p >= lo && p < te;
-    cidx[k] = live ? ld_stream(a.col + p, pol) : 0;
-    wv[k] = live ? ld_stream(a.val + p, pol) : 0.f;
+    cidx[k] = live ? ld_stream(colp + k * W, pol) : 0;
+    wv[k] = live ? ld_stream(valp + k * W, pol) : 0.f;
   }
-  for (int i = gl; i < cnt; i += W) {
-    wcrp[i] = a.crp[rbase + 1 + i];
-    wrid[i] = a.rid[rbase + i];
+  {
+    const int* const wsrc_crp = a.crp + (rbase + 1);
+    const int* const wsrc_rid = a.rid + rbase;
+#pragma unroll 1
+    for (int i = gl; i < cnt; i += W) {
+      wcrp[i] = wsrc_crp[(unsigned)i];
+      wrid[i] = wsrc_rid[(unsigned)i];
+    }
   }
   float xv[T][CT];
 #pragma unroll
   for (int k = 0; k < T; ++k) {
     const int p = tb + k * W + gl;
     const bool live = work && p >= lo && p < te;
-    load_dense_cols<CT>(a.X + (size_t)cidx[k] * N + col0, nt, vec, live, xv[k]);
+    load_dense_cols<CT>(xrow(cidx[k]), nt, vec, live, xv[k]);
   }
   __syncwarp();
 
@@ -164,7 +175,7 @@ par_ws_kernel(const ParArgs a) {
   // live lanes (they never feed a live lane's scan), and the last live lane
   // is flagged explicitly.  Dead lanes carry w = x = 0.
   char* const ybase = reinterpret_cast<char*>(a.Y + col0);
-  const long long ystride = (long long)N * 4;
+  const unsigned ystride = (unsigned)N * 4u;
   auto chunk = [&](bool en, int c0, float w, const float (&x)[CT]) {
     const int p = c0 + gl;
     const int hi = min(c0 + W, hard_end);
@@ -202,7 +213,7 @@ par_ws_kernel(const ParArgs a) {
       if (first_run && mode == MODE_ENTER_LONG) {
         store_cols<CT>(a.H + (size_t)(c0 / W) * N + col0, nt, t, false);
       } else if (rend <= c0 + W) {
-        store_cols<CT>(reinterpret_cast<float*>(ybase + (long long)wrid[ri] * ystride), nt, t, true);
+        store_cols<CT>(reinterpret_cast<float*>(ybase + (size_t)(unsigned)wrid[ri] * ystride), nt, t, true);
       }
     }
     // the last live run continuing past the chunk becomes the carried row
@@ -248,6 +259,7 @@ par_ws_kernel(const ParArgs a) {
     unsigned hw[T];
 #pragma unroll
     for (int k = 0; k < T; ++k) hw[k] = 0u;
+#pragma unroll 1
     for (int i = gl; i < cnt; i += W) {
       const int off = wcrp[i] - tb;
       if (off > 0 && off < T * W) {
@@ -307,7 +319,7 @@ par_ws_kernel(const ParArgs a) {
         if (first_run && mode == MODE_ENTER_LONG) {
           store_cols<CT>(a.H + (size_t)(c0 / W) * N + col0, nt, t, false);
         } else if (rend <= c0 + W) {
-          store_cols<CT>(reinterpret_cast<float*>(ybase + (long long)wrid[ri] * ystride), nt, t, true);
+          store_cols<CT>(reinterpret_cast<float*>(ybase + (size_t)(unsigned)wrid[ri] * ystride), nt, t, true);
         }
       }
       const int ll = max(min(hi - c0, W), 1) - 1;
@@ -346,7 +358,7 @@ par_ws_kernel(const ParArgs a) {
     const int ci = live ? ld_stream(a.col + p, pol) : 0;
     const float w = live ? ld_stream(a.val + p, pol) : 0.f;
     float x[CT];
-    load_dense_cols<CT>(a.X + (size_t)ci * N + col0, nt, vec, live, x);
+    load_dense_cols<CT>(xrow(ci), nt, vec, live, x);
     chunk(en, c0, w, x);
   }
 }

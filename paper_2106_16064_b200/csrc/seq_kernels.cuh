@@ -235,7 +235,9 @@ seq_kernel(const SeqArgs a) {
     for (int j = 0; j < B; ++j) {
       const int c = gshfl<LPU>(cr[j / LPU], j % LPU);
       if (eb + j < st.hard_end) {
-        st.cm.load(a.X + (size_t)c * st.N + st.col0, xv[j]);
+        st.cm.load(reinterpret_cast<const float*>(reinterpret_cast<const char*>(a.X + st.col0) +
+                                                  (size_t)(unsigned)c * ((unsigned)st.N * 4u)),
+                   xv[j]);
       } else {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) xv[j][k] = 0.f;
