@@ -79,6 +79,8 @@ struct SeqSweep {
   int* wcrp;  // wcrp[i] = crp[wb + 1 + i]
   int* wrid;  // wrid[i] = rid[wb + i]
   int gl, col0, N;
+  char* ybase;         // Y + col0: row address = ybase + row * ystride (32-bit math)
+  unsigned ystride;
   unsigned gmask;
   ColMap<LPU, CPL, VEC> cm;
 
@@ -116,6 +118,8 @@ struct SeqSweep {
     col0 = blockIdx.y * a.ncol_tile;
     cm = ColMap<LPU, CPL, VEC>{gl, min(a.ncol_tile, a.N - col0)};
     N = a.N;
+    ybase = reinterpret_cast<char*>(a.Y + col0);
+    ystride = (unsigned)a.N * 4u;
     const int4 d = a.desc[unit];
     cur = d.x;
     e = d.y;
@@ -158,7 +162,7 @@ struct SeqSweep {
         float o[CPL];
 #pragma unroll
         for (int k = 0; k < CPL; ++k) o[k] = __fadd_rn(carry[k], acc[k]);
-        cm.store(a.Y + (size_t)orow * N + col0, o);
+        cm.store(reinterpret_cast<float*>(ybase + (size_t)(unsigned)orow * ystride), o);
       }
       if (p >= te) {
         live = false;
@@ -427,124 +431,6 @@ seq_kernel_async(const SeqArgs a) {
       }
   }
   cp_async_wait<0>();
-}
-
-}  // namespace spmk_dev
-
-namespace spmk_dev {
-
-// --------------------------------------------------------------------------
-// Register-pipelined sweep for 4-aligned widths (every lane owns a float4 of
-// the column tile; LPU = column tile / 4 lanes per unit), the production
-// seq-rs / seq-ws kernel for N % 4 == 0.
-//   * colIdx/val of a batch of B nonzeros are loaded by every lane of the unit
-//     as 16-byte broadcast vectors (CSC: the sparse tile is
-//     read coalesced once per unit and shared by all its lanes), two batches
-//     ahead of consumption; dense-row float4 gathers one batch ahead, into
-//     registers through the L1-allocating read-only path, so hot dense rows
-//     of power-law matrices hit in L1.
-//   * loads are never predicated per element: the sweep runs over B-aligned
-//     batches; positions outside [e, hard_end) read harmless in-bounds data
-//     and are excluded from the sums (value 0 before e while acc is +0; the
-//     unit stops at its final event at hard_end).
-//   * events (row end / chunk boundary) are located per batch with one
-//     REDUX.OR over the units' next-event bits; the unrolled consume loop
-//     branches (warp-uniformly) only at positions where some unit has one.
-// EXACT: acc = acc + rn(v*x) (the reference's two roundings, bit-identical);
-// otherwise one FFMA per column (fast mode, within the stated tolerance).
-// --------------------------------------------------------------------------
-template <int LPU, int B, bool WS, bool EXACT>
-__global__ void __launch_bounds__(kSeqThreads, 2)
-seq4_kernel(const SeqArgs a) {
-  static_assert(B % 4 == 0 && B <= 16, "B");
-  using SW = SeqSweep<LPU, 4, true, WS>;
-  __shared__ int s_win[(kSeqThreads / LPU) * 2 * SW::WIN];
-  SW st;
-  st.setup_begin(a, s_win);
-  const uint64_t pol = evict_first_policy();
-  const int nnz = a.nnz;
-  const bool cvvec = a.cvvec != 0;
-  const int xoff = (4 * st.gl < st.cm.nt) ? 4 * st.gl : 0;  // idle lanes re-read column 0
-  const char* xg = reinterpret_cast<const char*>(a.X + st.col0 + xoff);
-  const long long xstride = (long long)a.N * 4;
-  const int ea = st.e & ~(B - 1);
-
-  auto load_cv = [&](int eb, int (&c)[B], float (&v)[B]) {
-    if (st.live && cvvec && eb + B <= nnz) {
-#pragma unroll
-      for (int i = 0; i < B; i += 4) {
-        const int4 ci = ld_stream4(a.col + eb + i, pol);
-        const float4 vi = ld_stream4(a.val + eb + i, pol);
-        c[i] = ci.x; c[i + 1] = ci.y; c[i + 2] = ci.z; c[i + 3] = ci.w;
-        v[i] = vi.x; v[i + 1] = vi.y; v[i + 2] = vi.z; v[i + 3] = vi.w;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < B; ++j) {
-        const int p = min(eb + j, nnz - 1);
-        const bool ok = st.live && eb + j < nnz;
-        c[j] = ok ? __ldg(a.col + p) : 0;
-        v[j] = ok ? __ldg(a.val + p) : 0.f;
-      }
-    }
-  };
-  auto load_x = [&](const int (&c)[B], float4 (&x)[B]) {
-#pragma unroll
-    for (int j = 0; j < B; ++j)
-      x[j] = __ldg(reinterpret_cast<const float4*>(xg + (long long)c[j] * xstride));
-  };
-
-  int cN[B], cNN[B];
-  float vC[B], vN[B], vNN[B];
-  float4 xC[B], xN[B];
-  {
-    int cC[B];
-    load_cv(ea, cC, vC);
-    load_cv(ea + B, cN, vN);
-    st.setup_end(a);
-#pragma unroll
-    for (int j = 0; j < B; ++j)
-      if (ea + j < st.e) vC[j] = 0.f;  // other rows' nonzeros before the unit start
-    load_x(cC, xC);
-  }
-
-#pragma unroll 1
-  for (int eb = ea; __any_sync(0xffffffffu, st.live); eb += B) {
-    load_x(cN, xN);
-    load_cv(eb + 2 * B, cNN, vNN);
-    auto next_bit = [&](int from) -> unsigned {
-      const int d = st.nev - eb;
-      return (st.live && d >= from && d < B) ? (1u << d) : 0u;
-    };
-    unsigned wm = __reduce_or_sync(0xffffffffu, next_bit(0));
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      if (wm & (1u << j)) {  // warp-uniform
-        if (st.live && st.nev == eb + j) st.event(a, eb + j);
-        wm = __reduce_or_sync(0xffffffffu, next_bit(j + 1));
-      }
-      const float v = vC[j];
-      const float4 x = xC[j];
-      if constexpr (EXACT) {
-        st.acc[0] = __fadd_rn(st.acc[0], __fmul_rn(v, x.x));
-        st.acc[1] = __fadd_rn(st.acc[1], __fmul_rn(v, x.y));
-        st.acc[2] = __fadd_rn(st.acc[2], __fmul_rn(v, x.z));
-        st.acc[3] = __fadd_rn(st.acc[3], __fmul_rn(v, x.w));
-      } else {
-        st.acc[0] = fmaf(v, x.x, st.acc[0]);
-        st.acc[1] = fmaf(v, x.y, st.acc[1]);
-        st.acc[2] = fmaf(v, x.z, st.acc[2]);
-        st.acc[3] = fmaf(v, x.w, st.acc[3]);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < B; ++j) {
-      xC[j] = xN[j];
-      vC[j] = vN[j];
-      cN[j] = cNN[j];
-      vN[j] = vNN[j];
-    }
-  }
 }
 
 }  // namespace spmk_dev

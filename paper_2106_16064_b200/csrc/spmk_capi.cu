@@ -335,25 +335,6 @@ void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   else launch_seq_async_nt<WS, B, S, 256>(a, lpu, tiles, s);
 }
 
-template <int LPU, int B, bool WS, bool EXACT>
-void launch_seq4_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
-  const int upb = 256 / LPU;
-  dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq4_kernel<LPU, B, WS, EXACT><<<grid, 256, 0, s>>>(a); LAUNCHED(1);
-}
-
-template <bool WS, int B, bool EXACT>
-void launch_seq4(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
-  switch (lpu) {
-    case 1: launch_seq4_t<1, B, WS, EXACT>(a, tiles, s); break;
-    case 2: launch_seq4_t<2, B, WS, EXACT>(a, tiles, s); break;
-    case 4: launch_seq4_t<4, B, WS, EXACT>(a, tiles, s); break;
-    case 8: launch_seq4_t<8, B, WS, EXACT>(a, tiles, s); break;
-    case 16: launch_seq4_t<16, B, WS, EXACT>(a, tiles, s); break;
-    default: launch_seq4_t<32, B, WS, EXACT>(a, tiles, s); break;
-  }
-}
-
 template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false>
 void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
@@ -392,23 +373,9 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     // ring below.  Other variants stay selectable for experiments.
     const long long variant = env_ll("SPMK_SEQ_VARIANT", lpu >= 8 ? 9 : 1);
     if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
-    else if (variant == 1) launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
     else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
-    else if (variant == 6) launch_seq_async<WS, 8, 4>(a, lpu, tiles, s);
-    else if (variant == 7) launch_seq_async<WS, 4, 4>(a, lpu, tiles, s);
-    else if (variant == 8) launch_seq_a2<WS, 8, 4, 128, true>(a, lpu, tiles, s);
     else if (variant == 9) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
-    else if (variant == 10) launch_seq_a2<WS, 4, 8, 128, true>(a, lpu, tiles, s);
-    else if (variant == 11) launch_seq_a2<WS, 8, 4, 128, false>(a, lpu, tiles, s);
-    else if (variant == 12) launch_seq_a2<WS, 8, 4, 256, true>(a, lpu, tiles, s);
-    else if (variant == 13) launch_seq_a2<WS, 8, 2, 128, true, true>(a, lpu, tiles, s);
-    else if (variant == 14) launch_seq_a2<WS, 8, 2, 256, true, true>(a, lpu, tiles, s);
-    else if (variant == 15) launch_seq_a2<WS, 8, 2, 256, true>(a, lpu, tiles, s);
-    else if (variant == 16) launch_seq_a2<WS, 16, 2, 128, true>(a, lpu, tiles, s);
-    else if (variant == 17 && lpu == 8) launch_seq_a2_t<8, 8, 2, WS, 128, true, false, false>(a, tiles, s);
-    else if (variant == 4) launch_seq4<WS, 8, false>(a, lpu, tiles, s);
-    else if (variant == 5) launch_seq4<WS, 4, true>(a, lpu, tiles, s);
-    else launch_seq4<WS, 8, true>(a, lpu, tiles, s);
+    else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
     const int lpu = next_pow2(N / 2);
     a.ncol_tile = 2 * lpu;

@@ -5,6 +5,7 @@ name=$1; kre=$2; shift 2
 ncu --set full --clock-control none --import-source on -k regex:"$kre" -s 1 -c 1 -o gpurun_out/$name "$@" > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/$name.ncu-rep > gpurun_out/${name}_summary.txt 2>&1
 python tools/ncu_hot.py gpurun_out/$name.ncu-rep 60 top > gpurun_out/${name}_hot.txt 2>&1
+python tools/ncu_hot.py gpurun_out/$name.ncu-rep 60 seq > gpurun_out/${name}_seq.txt 2>&1
 ncu -i gpurun_out/$name.ncu-rep --page raw --csv 2>/dev/null | python -c "
 import csv,sys
 r=list(csv.reader(sys.stdin)); h=r[0]

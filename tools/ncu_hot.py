@@ -23,7 +23,7 @@ print(f"total executed {tot_e}, samples {tot_s}, instructions {len(recs)}")
 mode = sys.argv[3] if len(sys.argv) > 3 else "seq"
 if mode == "seq":
     for e, s, a, src in recs:
-        if e >= tot_e / 2000 or s >= tot_s / 200:
+        if e >= tot_e / 20000 or s >= tot_s / 500:
             print(f"{a} {e:>10} {s:>6}  {src}")
 else:
     for e, s, a, src in sorted(recs, key=lambda r: -r[1])[:top]:
