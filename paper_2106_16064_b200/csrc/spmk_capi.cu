@@ -471,13 +471,10 @@ void launch_par_ws_tt(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
 
 void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   const int T = par_ws_chunks_per_tile();
-  // T = 4 measured best on B200 (R-MAT s20 heavy/uniform, N = 1 and 4)
-  const long long minb = env_ll("SPMK_PARWS_MINB", 5);
-  if (T == 8) launch_par_ws_tt<8, 1>(a, W, aligned, s);
-  else if (env_ll("SPMK_PARWS_V", 2) == 1) launch_par_ws_tt<4, 5, false>(a, W, aligned, s);
-  else if (minb == 5) launch_par_ws_tt<4, 5>(a, W, aligned, s);
-  else if (minb == 6) launch_par_ws_tt<4, 6>(a, W, aligned, s);
-  else launch_par_ws_tt<4, 4>(a, W, aligned, s);
+  // T = 4 chunks per tile, 5 blocks per SM: measured best on B200 (R-MAT
+  // s20 heavy/uniform, N = 1 and 4; T = 6 / 8 and 4 / 6 blocks were slower)
+  if (T == 8) launch_par_ws_tt<8, 4>(a, W, aligned, s);
+  else launch_par_ws_tt<4, 5>(a, W, aligned, s);
 }
 
 // Tile sizes (nonzeros per work unit).  Any multiple of the chunk keeps the
