@@ -456,7 +456,7 @@ void launch_par_ws_w(ParArgs a, bool aligned, cudaStream_t s) {
 
 // Tile shape of par-ws: T chunks of W nonzeros per group (a pure performance
 // knob: any T keeps the results bit-exact).
-int par_ws_chunks_per_tile() { return (int)env_ll("SPMK_PARWS_T", 4); }
+int par_ws_chunks_per_tile() { return env_ll("SPMK_PARWS_T", 4) == 8 ? 8 : 4; }  // the two compiled shapes
 
 template <int T, int MINB, bool BT = true>
 void launch_par_ws_tt(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
