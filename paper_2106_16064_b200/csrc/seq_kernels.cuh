@@ -456,7 +456,7 @@ constexpr int seq_async2_smem_bytes() {
 }
 
 template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA = false, bool LATE = false>
-__global__ void __launch_bounds__(NT, NT <= 128 ? 5 : 1)
+__global__ void __launch_bounds__(NT, NT <= 64 ? 10 : NT <= 128 ? 5 : 1)
 seq_async2_kernel(const SeqArgs a) {
   static_assert((S & (S - 1)) == 0 && S >= 2, "S must be a power of two");
   static_assert(B <= 16, "B");
