@@ -241,6 +241,25 @@ spmk_status spmk_pagerank_step(const float* d_y, float* d_r, const int32_t* d_co
                                int64_t m, int64_t m_total, double alpha, double* d_state,
                                double* d_scratch, double* d_hist, int32_t t, void* stream);
 
+/* Fused update + exchange for the row-partitioned iterative SpMV (one rank
+ * of a multi-GPU run): for i < m, x_next[row0 + i] = alpha*y[i] + d_state[0]
+ * is stored into every buffer of peer_x_next[0..npeers) (HOST array of device
+ * pointers: this GPU's own x_next and its peers' buffers mapped with
+ * spmk_ipc_open, written with P2P stores over NVLink), with the same
+ * fixed-order reductions as spmk_pagerank_step (residual against d_x_cur,
+ * dangling mass; d_counts and both x vectors are indexed globally).  npeers
+ * <= 8.  The replicas are complete once every rank's call has finished. */
+spmk_status spmk_pagerank_step_p2p(const float* d_y, const float* d_x_cur,
+                                   float* const* peer_x_next, int32_t npeers,
+                                   const int32_t* d_counts, int64_t row0, int64_t m,
+                                   int64_t m_total, double alpha, double* d_state,
+                                   double* d_scratch, void* stream);
+/* CUDA IPC for the peer buffers above: 64-byte handle of a device
+ * allocation, open a peer's handle (lazy peer access), close it. */
+spmk_status spmk_ipc_handle(const void* d_ptr, void* handle64);
+spmk_status spmk_ipc_open(const void* handle64, void** d_ptr);
+spmk_status spmk_ipc_close(void* d_ptr);
+
 /* ------------------------------------------------------------ generators */
 /* generate_rmat<float> (rmat.hpp:61-88 + csr.hpp:123-164) on the device,
  * bit-identical to the reference (counter form of SplitMix64): returns a

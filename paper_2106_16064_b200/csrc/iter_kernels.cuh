@@ -83,6 +83,54 @@ pagerank_update_kernel(const float* __restrict__ y, float* __restrict__ r, const
   }
 }
 
+// Fused update + exchange of the row-partitioned iterative SpMV: this rank's
+// slice x_next[row0 + i] = alpha*y[i] + base is stored into every replica of
+// x_next — this GPU's own and its peers' (CUDA-IPC-mapped buffers reached
+// over NVLink with plain P2P stores) — in the same pass that computes the
+// residual against x_cur and the dangling mass.  The replicas are complete
+// once every rank's kernel has finished (the residual all-reduce that follows
+// is the barrier), so no separate all-gather is needed.
+constexpr int kMaxPeers = 8;
+struct PeerPtrs {
+  float* p[kMaxPeers];
+};
+__global__ void __launch_bounds__(kIterThreads)
+pagerank_update_p2p_kernel(const float* __restrict__ y, const float* __restrict__ xcur,
+                           const int* __restrict__ counts, long long row0, long long m, float alpha,
+                           const double* __restrict__ st, PeerPtrs peers, int npeers,
+                           double* __restrict__ part) {
+  __shared__ double s1[kIterThreads / 32], s2[kIterThreads / 32];
+  const float base = (float)st[0];
+  double l1 = 0.0, dang = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    float rv = xcur[row0 + i];  // old value in, new value out (residual inside)
+    pr_elem(y[i], rv, counts[row0 + i], alpha, base, l1, dang);
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q < npeers) peers.p[q][row0 + i] = rv;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    dang += __shfl_xor_sync(0xffffffffu, dang, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s1[threadIdx.x >> 5] = l1;
+    s2[threadIdx.x >> 5] = dang;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < kIterThreads / 32; ++w) {
+      a += s1[w];
+      b += s2[w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
 // Ordered sum of the block partials; st = {base for the next step, l1,
 // dangling mass}; hist[t] = l1 of step t.  One warp, fixed order.
 __global__ void pagerank_finalize_kernel(const double* __restrict__ part, int nblocks, long long m_total,

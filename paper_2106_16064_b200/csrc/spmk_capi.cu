@@ -1353,6 +1353,50 @@ spmk_status spmk_pagerank_step(const float* d_y, float* d_r, const int32_t* d_co
   return e == cudaSuccess ? SPMK_OK : fail(SPMK_ECUDA, cudaGetErrorString(e));
 }
 
+spmk_status spmk_pagerank_step_p2p(const float* d_y, const float* d_x_cur, float* const* peer_x_next,
+                                   int32_t npeers, const int32_t* d_counts, int64_t row0, int64_t m,
+                                   int64_t m_total, double alpha, double* d_state, double* d_scratch,
+                                   void* stream) {
+  if (!d_y || !d_x_cur || !peer_x_next || !d_counts || !d_state || !d_scratch || m < 0 || m_total < 1 ||
+      row0 < 0 || npeers < 1 || npeers > kMaxPeers)
+    return fail(SPMK_EINVAL, "bad argument");
+  PeerPtrs pp{};
+  for (int q = 0; q < npeers; ++q) {
+    if (!peer_x_next[q]) return fail(SPMK_EINVAL, "null peer buffer");
+    pp.p[q] = peer_x_next[q];
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  pagerank_update_p2p_kernel<<<kIterBlocks, kIterThreads, 0, s>>>(d_y, d_x_cur, d_counts, row0, m, (float)alpha,
+                                                                  d_state, pp, npeers, d_scratch); LAUNCHED(1);
+  pagerank_finalize_kernel<<<1, 32, 0, s>>>(d_scratch, kIterBlocks, m_total, alpha, d_state, nullptr, 0); LAUNCHED(1);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SPMK_OK : fail(SPMK_ECUDA, cudaGetErrorString(e));
+}
+
+spmk_status spmk_ipc_handle(const void* d_ptr, void* handle64) {
+  if (!d_ptr || !handle64) return fail(SPMK_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr));
+  if (e != cudaSuccess) return fail(SPMK_ECUDA, cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  std::memcpy(handle64, &h, 64);
+  return SPMK_OK;
+}
+
+spmk_status spmk_ipc_open(const void* handle64, void** d_ptr) {
+  if (!handle64 || !d_ptr) return fail(SPMK_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(SPMK_ECUDA, cudaGetErrorString(e));
+  return SPMK_OK;
+}
+
+spmk_status spmk_ipc_close(void* d_ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  return e == cudaSuccess ? SPMK_OK : fail(SPMK_ECUDA, cudaGetErrorString(e));
+}
+
 uint64_t spmk_launch_count(void) { return g_launches.load(); }
 
 spmk_status spmk_timing_enable(int on) {

@@ -152,16 +152,38 @@ def exchange_slices(x, bounds: List[int], group=None) -> None:
             dist.broadcast(x[lo:hi], src=g, group=group)
 
 
+def _ipc_handle(t) -> bytes:
+    buf = (C.c_char * 64)()
+    _check(_lib().spmk_ipc_handle(vp(t.data_ptr()), C.cast(buf, vp)))
+    return bytes(buf)
+
+
+def _ipc_open(handle: bytes) -> int:
+    buf = (C.c_char * 64).from_buffer_copy(handle)
+    out = vp()
+    _check(_lib().spmk_ipc_open(C.cast(buf, vp), C.byref(out)))
+    return out.value
+
+
 class DistributedPageRank:
     """One rank of the row-partitioned iterative SpMV.  ``full`` is the whole
-    square A on this rank's GPU (each rank keeps only its slice afterwards)."""
+    square A on this rank's GPU (each rank keeps only its slice afterwards).
 
-    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None):
+    exchange="nccl": update this rank's slice of x in place, then one NCCL
+    broadcast per rank (unequal slices).  exchange="p2p": x is double-buffered
+    and every rank's update kernel stores its slice of x_next straight into
+    all ranks' replicas (CUDA-IPC-mapped peer buffers, P2P over NVLink) —
+    update and all-gather fused into one kernel; the residual all-reduce that
+    follows is the barrier before the next SpMV reads x_next."""
+
+    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None, exchange: str = "nccl"):
         import torch
         import torch.distributed as dist
 
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.group, self.alpha, self.m = group, float(alpha), full.num_rows
+        self.group, self.alpha, self.m, self.exchange = group, float(alpha), full.num_rows, exchange
         dev = torch.cuda.current_device()
         self.bounds = [int(b) for b in full.row_slices(self.world)]
         lo, hi = self.bounds[self.rank], self.bounds[self.rank + 1]
@@ -172,10 +194,41 @@ class DistributedPageRank:
         self.counts = counts
         make_column_stochastic(self.a, counts)
         self.kid = self.a.select(1)
-        self.x = torch.full((self.m, 1), 1.0 / self.m, dtype=torch.float32, device="cuda")
         self.y = torch.empty((hi - lo, 1), dtype=torch.float32, device="cuda")
         self.state = torch.zeros(3, dtype=torch.float64, device="cuda")
         self.scratch = torch.empty(int(_lib().spmk_pagerank_scratch_doubles()), dtype=torch.float64, device="cuda")
+        self.xbuf = [torch.full((self.m, 1), 1.0 / self.m, dtype=torch.float32, device="cuda")]
+        self.cur = 0
+        self.opened: List[int] = []
+        if exchange == "p2p":
+            if self.world > 8:
+                raise ValueError("p2p exchange supports up to 8 ranks")
+            self.xbuf.append(torch.empty_like(self.xbuf[0]))
+            torch.cuda.synchronize()
+            self.peers = []
+            for b in range(2):
+                mine = _ipc_handle(self.xbuf[b])
+                handles = [None] * self.world
+                dist.all_gather_object(handles, mine, group=group)
+                ptrs = []
+                for r in range(self.world):
+                    if r == self.rank:
+                        ptrs.append(self.xbuf[b].data_ptr())
+                    else:
+                        p = _ipc_open(handles[r])
+                        self.opened.append(p)
+                        ptrs.append(p)
+                self.peers.append((vp * self.world)(*ptrs))
+            dist.barrier(group=group)
+
+    @property
+    def x(self):
+        return self.xbuf[self.cur]
+
+    def close(self):
+        for p in self.opened:
+            _lib().spmk_ipc_close(vp(p))
+        self.opened = []
 
     def _global_base(self):
         import torch.distributed as dist
@@ -187,28 +240,45 @@ class DistributedPageRank:
 
     def reset(self):
         import torch
+        import torch.distributed as dist
 
-        self.x.fill_(1.0 / self.m)
+        for b in self.xbuf:
+            b.fill_(1.0 / self.m)
+        self.cur = 0
         st = torch.cuda.current_stream()
         _check(_lib().spmk_pagerank_init(vp(self.x[self.lo:self.hi].data_ptr()),
                                          vp(self.counts[self.lo:].data_ptr()), self.hi - self.lo, self.m,
                                          C.c_double(self.alpha), vp(self.state.data_ptr()),
                                          vp(self.scratch.data_ptr()), vp(st.cuda_stream)))
         self._global_base()
+        if self.exchange == "p2p":
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)  # every replica initialised before peers write
 
     def step(self):
         import torch
 
         st = torch.cuda.current_stream()
+        x = self.x
         if self.hi > self.lo:
-            self.a.spmm(self.kid, self.x, self.y, stream=st)
-        xs = self.x[self.lo:self.hi]
+            self.a.spmm(self.kid, x, self.y, stream=st)
+        if self.exchange == "p2p":
+            nxt = 1 - self.cur
+            _check(_lib().spmk_pagerank_step_p2p(vp(self.y.data_ptr()), vp(x.data_ptr()), self.peers[nxt],
+                                                 self.world, vp(self.counts.data_ptr()), self.lo,
+                                                 self.hi - self.lo, self.m, C.c_double(self.alpha),
+                                                 vp(self.state.data_ptr()), vp(self.scratch.data_ptr()),
+                                                 vp(st.cuda_stream)))
+            self._global_base()  # all-reduce: also the barrier before x_next is read
+            self.cur = nxt
+            return
+        xs = x[self.lo:self.hi]
         _check(_lib().spmk_pagerank_step(vp(self.y.data_ptr()), vp(xs.data_ptr()),
                                          vp(self.counts[self.lo:].data_ptr()), self.hi - self.lo, self.m,
                                          C.c_double(self.alpha), vp(self.state.data_ptr()),
                                          vp(self.scratch.data_ptr()), vp(0), 0, vp(st.cuda_stream)))
         self._global_base()
-        exchange_slices(self.x.view(-1), self.bounds, self.group)
+        exchange_slices(x.view(-1), self.bounds, self.group)
 
     def run(self, iters: int = 50):
         self.reset()

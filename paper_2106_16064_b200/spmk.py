@@ -98,6 +98,10 @@ _SIGS = {
     "spmk_pagerank_scratch_doubles": ([], i64),
     "spmk_pagerank_init": ([vp, vp, i64, i64, f64, vp, vp, vp], C.c_int),
     "spmk_pagerank_step": ([vp, vp, vp, i64, i64, f64, vp, vp, vp, C.c_int32, vp], C.c_int),
+    "spmk_pagerank_step_p2p": ([vp, vp, P(vp), C.c_int32, vp, i64, i64, i64, f64, vp, vp, vp], C.c_int),
+    "spmk_ipc_handle": ([vp, vp], C.c_int),
+    "spmk_ipc_open": ([vp, P(vp)], C.c_int),
+    "spmk_ipc_close": ([vp], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -82,5 +82,12 @@ def test_distributed_driver_single_rank_matches(graph, orc):
         x, _ = dp.run(10)
         x1, _ = pr.run(10, graph=False)
         assert np.array_equal(x.cpu().numpy(), x1.cpu().numpy())
+        # fused update + exchange (P2P stores into every replica; here the
+        # rank's own buffer) computes the same iterates bit for bit
+        d3 = spmk.DeviceCsr.generate_rmat(12, 8, (0.57, 0.19, 0.19, 0.05), 3)
+        dq = prk.DistributedPageRank(d3, ALPHA, exchange="p2p")
+        xq, hq = dq.run(10)
+        assert np.array_equal(xq.cpu().numpy(), x1.cpu().numpy())
+        dq.close()
     finally:
         dist.destroy_process_group()
