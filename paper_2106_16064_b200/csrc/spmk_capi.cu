@@ -335,18 +335,18 @@ void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   else launch_seq_async_nt<WS, B, S, 256>(a, lpu, tiles, s);
 }
 
-template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false>
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false, bool UNR = true>
 void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
   static bool attr_set = false;
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE>,
+    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
+  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
 }
 
 template <bool WS, int B, int S, int NT, bool EXACT, bool CA = false>
@@ -375,6 +375,7 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
     else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
     else if (variant == 9) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
+    else if (variant == 13 && lpu == 8) launch_seq_a2_t<8, 8, 2, WS, 128, true, false, false, false>(a, tiles, s);
 
     else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
