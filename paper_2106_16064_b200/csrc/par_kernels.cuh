@@ -75,27 +75,37 @@ par_rs_kernel(const ParArgs a) {
       w[v] = live ? ld_stream(a.val + p, pol) : 0.f;
     }
   };
-  auto accumulate = [&](const int (&c)[VL], const float (&w)[VL], float (&acc)[CT], float (&acc2)[VL == 2 ? CT : 1]) {
+  const char* const xb = reinterpret_cast<const char*>(a.X + col0);
+  const unsigned xs = (unsigned)N * 4u;
+  // dense-row loads of one batch (issued before any of the batch's FMAs)
+  auto load_x = [&](const int (&c)[VL], float (&xv)[VL][CT]) {
+#pragma unroll
+    for (int v = 0; v < VL; ++v) {
+      const float* xr = reinterpret_cast<const float*>(xb + (size_t)(unsigned)max(c[v], 0) * xs);
+      const bool ok = c[v] >= 0;
+      if constexpr (VEC4 && CT % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < CT; k += 4) {
+          if (ok && k < nt) {
+            const float4 t = ld_x4(xr + k);
+            xv[v][k] = t.x; xv[v][k + 1] = t.y; xv[v][k + 2] = t.z; xv[v][k + 3] = t.w;
+          } else {
+            xv[v][k] = xv[v][k + 1] = xv[v][k + 2] = xv[v][k + 3] = 0.f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < CT; ++k) xv[v][k] = (ok && k < nt) ? ld_x(xr + k) : 0.f;
+      }
+    }
+  };
+  // lane-sequential FMA chain (kernels.hpp:181-186); dead lanes add nothing
+  auto fma_batch = [&](const int (&c)[VL], const float (&w)[VL], const float (&xall)[VL][CT], float (&acc)[CT],
+                       float (&acc2)[VL == 2 ? CT : 1]) {
 #pragma unroll
     for (int v = 0; v < VL; ++v) {
       if (c[v] >= 0) {
-        const float* xr = reinterpret_cast<const float*>(
-            reinterpret_cast<const char*>(a.X + col0) + (size_t)(unsigned)c[v] * ((unsigned)N * 4u));
-        float xv[CT];
-        if constexpr (VEC4 && CT % 4 == 0) {
-#pragma unroll
-          for (int k = 0; k < CT; k += 4) {
-            if (k < nt) {
-              const float4 t = ld_x4(xr + k);
-              xv[k] = t.x; xv[k + 1] = t.y; xv[k + 2] = t.z; xv[k + 3] = t.w;
-            } else {
-              xv[k] = xv[k + 1] = xv[k + 2] = xv[k + 3] = 0.f;
-            }
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < CT; ++k) xv[k] = (k < nt) ? ld_x(xr + k) : 0.f;
-        }
+        const float (&xv)[CT] = xall[v];
         if constexpr (VL == 2) {
           if (v == 1) {
 #pragma unroll
@@ -132,17 +142,30 @@ par_rs_kernel(const ParArgs a) {
     float acc2[VL == 2 ? CT : 1];
 #pragma unroll
     for (int k = 0; k < (VL == 2 ? CT : 1); ++k) acc2[k] = 0.f;
-    accumulate(c0, w0, acc, acc2);
-    for (int base = s + W; base < f; base += W) {  // rows longer than W
-      int c[VL];
-      float w[VL];
+    {
+      float x0[VL][CT];
+      load_x(c0, x0);
+      fma_batch(c0, w0, x0, acc, acc2);
+    }
+    // rows longer than W: U batches of colIdx/val, then their dense rows, are
+    // in flight before the (in-order) FMAs of the first one
+    constexpr int U = CT <= 1 ? 4 : (CT <= 4 ? 2 : 1);
+    for (int base = s + W; base < f; base += U * W) {
+      int c[U][VL];
+      float w[U][VL];
 #pragma unroll
-      for (int v = 0; v < VL; ++v) {
-        const int p = base + gl * VL + v;
-        c[v] = p < f ? ld_stream(a.col + p, pol) : -1;
-        w[v] = p < f ? ld_stream(a.val + p, pol) : 0.f;
-      }
-      accumulate(c, w, acc, acc2);
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < VL; ++v) {
+          const int p = base + u * W + gl * VL + v;
+          c[u][v] = p < f ? ld_stream(a.col + p, pol) : -1;
+          w[u][v] = p < f ? ld_stream(a.val + p, pol) : 0.f;
+        }
+      float xv[U][VL][CT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) load_x(c[u], xv[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) fma_batch(c[u], w[u], xv[u], acc, acc2);
     }
     if constexpr (VL == 2) {
       // tree level 1 of the 64-lane model: acc[l] = acc[2l+1] + acc[2l]

@@ -375,7 +375,7 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
     else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
     else if (variant == 9) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
-    else if (variant == 13 && lpu == 8) launch_seq_a2_t<8, 8, 2, WS, 128, true, false, false, false>(a, tiles, s);
+
 
     else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
