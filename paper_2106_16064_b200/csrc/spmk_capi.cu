@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/spmk_capi.h"
@@ -279,6 +280,17 @@ long long env_ll(const char* name, long long dflt) {
   return v ? std::atoll(v) : dflt;
 }
 
+// The dynamic-shared-memory opt-in is per (kernel, device): remember which
+// pairs have it so multi-device processes set it on every device.
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, bool> g_attr_done;
+bool need_smem_attr(const void* fn) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  return !std::exchange(g_attr_done[{fn, dev}], true);
+}
+
 // ------------------------------------------------------------ seq launch
 template <int LPU, int CPL, bool VEC, int B, bool WS>
 void launch_seq_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
@@ -305,11 +317,8 @@ void launch_seq_lpu(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
 template <int LPU, int B, int S, bool WS, int NT>
 void launch_seq_async_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async_smem_bytes<LPU, B, S, NT>();
-  static bool attr_set = false;  // per instantiation (host-side, benign race)
-  if (!attr_set) {
+  if (need_smem_attr(reinterpret_cast<const void*>(seq_kernel_async<LPU, B, S, WS, NT>)))
     CK(cudaFuncSetAttribute(seq_kernel_async<LPU, B, S, WS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
   const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
   seq_kernel_async<LPU, B, S, WS, NT><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
@@ -338,12 +347,9 @@ void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
 template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false, bool UNR = true>
 void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (need_smem_attr(reinterpret_cast<const void*>(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR>)))
     CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
-  }
   const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
   seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
