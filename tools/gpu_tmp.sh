@@ -1,1 +1,2 @@
-timeout 300 python tools/probe_perf.py --scale 20 --ef 16 --ns 5,6,7,8,12,24 2>&1 | grep "seq-ws\|par-ws"
+timeout 300 python tools/bench_cfg1.py 2>&1 | tail -2
+timeout 300 python bench.py --impl reference --scale 16 --steps 5 --warmup 2 2>&1 | tail -1
