@@ -378,9 +378,9 @@ seq_kernel_async(const SeqArgs a) {
   float vring[R][SLOTS];
 #pragma unroll
   for (int r = 0; r < R - 1; ++r) load_cv(st.e + r * B, cring[r], vring[r]);
-  st.setup_end(a);
 #pragma unroll
   for (int s = 0; s < S - 1; ++s) issue(st.e + s * B, s, cring[s]);
+  st.setup_end(a);
 
   int stage = 0;
 #pragma unroll 1
@@ -514,9 +514,10 @@ seq_async2_kernel(const SeqArgs a) {
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
     if (ea + s * LPU + st.gl < st.e) vring[0][s] = 0.f;  // other rows before the unit start
-  st.setup_end(a);
+  // first gathers before the row window: its loads then overlap them
 #pragma unroll
   for (int i = 0; i < S - 1; ++i) issue(i, cring[i]);
+  st.setup_end(a);
 
   int stage = 0;
 #pragma unroll 1
