@@ -1,0 +1,77 @@
+"""C-ABI behaviours beyond the kernels: asynchronous host-operand calls on two
+streams (rotating staging slots), |A| handle copy, calls on distinct streams
+of one handle, unaligned dense operands, and the error paths."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2106_16064_b200 as spmk  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mat():
+    return spmk.DeviceCsr.generate_rmat(12, 8, (0.57, 0.19, 0.19, 0.05), 11)
+
+
+def test_async_host_calls_on_two_streams(mat):
+    kid = mat.select(16)
+    xs = [torch.randn(mat.num_cols, 16).pin_memory() for _ in range(4)]
+    ys = [torch.empty(mat.num_rows, 16).pin_memory() for _ in range(4)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for i in range(4):
+        mat.spmm_host_async(kid, xs[i].numpy(), ys[i].numpy(), streams[i % 2].cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(4):
+        want = mat.spmm(kid, xs[i].cuda()).cpu()
+        assert torch.equal(ys[i], want), i
+
+
+def test_abs_copy(mat):
+    h = mat.download()
+    a2 = mat.abs_copy()
+    h2 = a2.download()
+    assert np.array_equal(h2.row_ptr, h.row_ptr) and np.array_equal(h2.col_idx, h.col_idx)
+    assert np.array_equal(h2.values, np.abs(h.values))
+
+
+def test_concurrent_streams_same_handle(mat):
+    x = torch.randn(mat.num_cols, 8, device="cuda")
+    ref = {k.name: mat.spmm(k, x).clone() for k in spmk.kAllKernels}
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = {}
+    for s, k in zip(streams, spmk.kAllKernels):
+        with torch.cuda.stream(s):
+            outs[k.name] = mat.spmm(k, x, stream=s)
+    torch.cuda.synchronize()
+    for name, y in outs.items():
+        assert torch.equal(y, ref[name]), name
+
+
+def test_unaligned_dense_operands(mat):
+    """X and Y at 4-byte (not 16-byte) offsets take the scalar paths and give
+    the same bits."""
+    n = 8
+    xb = torch.randn(mat.num_cols * n + 1, device="cuda")
+    x_un = xb[1:].view(mat.num_cols, n)
+    x_al = x_un.clone()
+    yb = torch.empty(mat.num_rows * n + 1, device="cuda")
+    y_un = yb[1:].view(mat.num_rows, n)
+    for k in spmk.kAllKernels:
+        mat.spmm(k, x_un, y_un)
+        assert torch.equal(y_un, mat.spmm(k, x_al)), k.name
+
+
+def test_error_paths(mat):
+    x = torch.randn(mat.num_cols + 1, 4, device="cuda")
+    with pytest.raises(spmk.Error):
+        mat.spmm(spmk.kSeqBalanced, x)  # dimension mismatch
+    with pytest.raises(spmk.Error):
+        spmk.check_config(spmk.KernelConfig(lane_width=3))
+    with pytest.raises(spmk.UnsupportedError):
+        mat.spmm(spmk.kParBalanced, torch.randn(mat.num_cols, 4, device="cuda"),
+                 cfg=spmk.KernelConfig(lane_width=64))
+    with pytest.raises(spmk.Error):
+        spmk.DeviceCsr.generate_rmat(0, 8)
