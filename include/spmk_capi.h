@@ -163,7 +163,11 @@ spmk_status spmk_row_slices(spmk_csr_t a, int64_t parts, int64_t* bounds);
  * Y is fully overwritten (empty rows get 0).  cfg may be NULL (defaults).
  * Asynchronous on `stream` (NULL = legacy default stream).  Results are
  * bit-identical to the reference's fp32 kernel of the same KernelId at the
- * same lane_width / seq_chunk (same partials, same summation order). */
+ * same lane_width / seq_chunk (same partials, same summation order).
+ * A handle's calls on different streams are ordered (a call waits for the
+ * previous call's kernels when it arrives on another stream: they share the
+ * handle's partial-slot scratch and side stream); calls captured into a CUDA
+ * graph are not, so replay such a graph on the capturing stream. */
 spmk_status spmk_spmm(spmk_csr_t a, spmk_kernel_id id,
                       const spmk_kernel_config* cfg, const float* d_x,
                       int64_t n, float* d_y, void* stream);

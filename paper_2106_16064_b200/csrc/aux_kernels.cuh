@@ -169,11 +169,11 @@ __global__ void ws_tile_desc_kernel(const int* __restrict__ crp, const int* __re
     desc[t] = make_int4(cur, (int)start, (int)hard_end, mode);
   }
 }
-__global__ void rs_tile_desc_kernel(const int* __restrict__ crp, int mne, int RB, long long ntiles,
+__global__ void rs_tile_desc_kernel(const int* __restrict__ crp, const int* __restrict__ rlo, long long ntiles,
                                     int4* __restrict__ desc) {
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ntiles;
        t += (long long)gridDim.x * blockDim.x) {
-    const int r0 = (int)(t * RB), r1 = min(r0 + RB, mne);
+    const int r0 = rlo[t], r1 = rlo[t + 1];
     desc[t] = make_int4(r0, crp[r0], crp[r1], MODE_NORMAL);
   }
 }

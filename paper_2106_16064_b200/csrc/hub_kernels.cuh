@@ -1,0 +1,195 @@
+// Hub rows of the row-split variants (par-rs, seq-rs).
+//
+// The row-split variants give one worker to one row (kernels.hpp:157-224 and
+// :339-376): a row's sum is a single ordered chain (seq-rs) or W per-lane
+// chains plus a fixed tree (par-rs).  On power-law matrices one group then
+// serialises a 40K-nonzero row behind ~2 dependent memory round trips per
+// step.  Rows with >= L nonzeros ("hubs", plan-time list) are skipped by the
+// main row-split kernels and computed here instead, one CTA per (hub row,
+// column tile), in exactly the reference's order:
+//
+//   * seq-rs: products v*x (rounded) are formed in parallel by 7 producer
+//     warps into a double-buffered shared-memory chunk while warp 0 folds
+//     the previous chunk in position order (acc += p; one chain per column).
+//     The chain is then the only serial part: ~4 cycles per nonzero.
+//   * par-rs: one thread per (lane chain l, column): chain l sums positions
+//     s + l + j*W in j order with 16 steps of gathers in flight; the tree
+//     acc[l] = acc[2l+1] + acc[2l] (kernels.hpp:193-199) runs per column
+//     from shared memory.
+#pragma once
+
+#include "common.cuh"
+
+namespace spmk_dev {
+
+constexpr int kHubThreads = 256;
+constexpr int kHubProducers = 7;                // seq-rs: warps 1..7 form products
+constexpr int kHubChunk = kHubProducers * 32;   // positions per shared-memory chunk
+template <int CW>
+constexpr int hub_smem_bytes() { return 2 * kHubChunk * CW * 4; }  // double buffer (57,344 B at CW = 32)
+
+// Rows with >= L nonzeros: {compact row, length}.
+__global__ void hub_rows_kernel(const int* __restrict__ crp, int mne, int L, int2* __restrict__ out,
+                                int* __restrict__ count) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < mne;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int len = crp[c + 1] - crp[c];
+    if (len >= L) out[atomicAdd(count, 1)] = make_int2((int)c, len);
+  }
+}
+
+struct HubArgs {
+  const int* __restrict__ hubs;  // compact rows, longest first
+  const int* __restrict__ crp;
+  const int* __restrict__ rid;
+  const int* __restrict__ col;
+  const float* __restrict__ val;
+  const float* __restrict__ X;
+  float* __restrict__ Y;
+  int N;
+};
+
+// seq-rs (kernels.hpp:339-376): acc = 0; for e in row: acc += val[e]*x[col[e]].
+// CW columns per CTA (power of two <= 32); a producer lane (sg, cl) gathers
+// positions sg + (32/CW)*t of its warp's 32, so small N wastes no lanes.
+// Producers run two chunks ahead in registers (colIdx/val) and one chunk
+// ahead in flight (the gathers), so each barrier interval costs about one
+// fold of kHubChunk dependent adds.
+template <int CW>
+__global__ void __launch_bounds__(kHubThreads, 1) seq_rs_hub_kernel(const HubArgs a) {
+  constexpr int SG = 32 / CW;
+  extern __shared__ float hub_buf[];  // [2][kHubChunk][CW]
+  const int r = a.hubs[blockIdx.x];
+  const int s = a.crp[r], f = a.crp[r + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sg = lane / CW, cl = lane % CW;
+  const int c = blockIdx.y * CW + cl;
+  const bool cok = c < a.N;
+  const int cx = min(c, a.N - 1);  // gathers are unpredicated (a dead slot is never folded)
+  const unsigned xs = (unsigned)a.N;
+  const int nch = (f - s + kHubChunk - 1) / kHubChunk;
+  const int pw = warp - 1;
+  auto ldcv = [&](int it, int& cc, float& vv) {
+    const int p = s + it * kHubChunk + pw * 32 + lane;
+    cc = p < f ? a.col[p] : 0;
+    vv = p < f ? a.val[p] : 0.f;
+  };
+  // Plain loads into registers consumed one barrier interval later: no
+  // select on the loaded value, so all CW gathers stay in flight.
+  auto gather = [&](int cc, float (&xv)[CW]) {
+#pragma unroll
+    for (int t = 0; t < CW; ++t) {
+      const int ci = __shfl_sync(0xffffffffu, cc, sg + SG * t);
+      xv[t] = ld_x(a.X + (size_t)(unsigned)ci * xs + cx);
+    }
+  };
+  int cc0 = 0, cc1 = 0;
+  float vv0 = 0.f, vv1 = 0.f;
+  float xv[CW];
+  if (warp > 0) {
+    ldcv(0, cc0, vv0);
+    ldcv(1, cc1, vv1);
+    gather(cc0, xv);
+  }
+  float acc = 0.f;
+  for (int it = 0; it <= nch; ++it) {
+    if (warp > 0) {
+      if (it < nch) {
+        float* b = hub_buf + (it & 1) * kHubChunk * CW + pw * 32 * CW;
+#pragma unroll
+        for (int t = 0; t < CW; ++t) {
+          const int i = sg + SG * t;
+          b[i * CW + cl] = __fmul_rn(__shfl_sync(0xffffffffu, vv0, i), xv[t]);
+        }
+        cc0 = cc1;
+        vv0 = vv1;
+        if (it + 1 < nch) gather(cc0, xv);
+        ldcv(it + 2, cc1, vv1);
+      }
+    } else if (it > 0 && lane < CW) {
+      const float* b = hub_buf + ((it - 1) & 1) * kHubChunk * CW + cl;
+      const int cnt = min(kHubChunk, f - s - (it - 1) * kHubChunk);
+      if (cnt == kHubChunk && CW >= 16) {
+#pragma unroll 16
+        for (int i = 0; i < kHubChunk; ++i) acc = __fadd_rn(acc, b[i * CW]);
+      } else if (cnt == kHubChunk) {
+        // 32 products per batch, the next batch's shared-memory loads issued
+        // before this batch's adds: the add chain never waits on LDS latency
+        float nx[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) nx[k] = b[k * CW];
+#pragma unroll 1
+        for (int bb = 0; bb < kHubProducers; ++bb) {
+          float cur[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) cur[k] = nx[k];
+          if (bb + 1 < kHubProducers) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) nx[k] = b[((bb + 1) * 32 + k) * CW];
+          }
+#pragma unroll
+          for (int k = 0; k < 32; ++k) acc = __fadd_rn(acc, cur[k]);
+        }
+      } else {
+#pragma unroll 4
+        for (int i = 0; i < cnt; ++i) acc = __fadd_rn(acc, b[i * CW]);
+      }
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && lane < CW && cok) a.Y[(size_t)(unsigned)a.rid[r] * xs + c] = acc;
+}
+
+// par-rs (kernels.hpp:157-224) with W lanes: thread (l, cl) of a W x CW CTA
+// owns lane chain l (positions s + l + j*W, in j order) of column cl; U steps
+// of colIdx/val are loaded one batch ahead so a batch costs one gather round
+// trip.  Then the tree acc[l] = acc[2l+1] + acc[2l] (kernels.hpp:193-199).
+__global__ void __launch_bounds__(kHubThreads) par_rs_hub_kernel(const HubArgs a, int W, int CW) {
+  constexpr int U = 16;
+  __shared__ float sacc[kHubThreads];
+  const int t = threadIdx.x;
+  const int l = t / CW, cl = t % CW;
+  const int r = a.hubs[blockIdx.x];
+  const int s = a.crp[r], f = a.crp[r + 1];
+  const int c = blockIdx.y * CW + cl;
+  const bool cok = c < a.N;
+  const int cx = min(c, a.N - 1);
+  const unsigned xs = (unsigned)a.N;
+  int cc[U];
+  float vv[U];
+  auto load = [&](int p) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = p + u * W;
+      cc[u] = q < f ? a.col[q] : 0;
+      vv[u] = q < f ? a.val[q] : 0.f;
+    }
+  };
+  float acc = 0.f;
+  int p = s + l;
+  load(p);
+  for (; p < f; p += U * W) {
+    float xv[U], vc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      vc[u] = vv[u];
+      xv[u] = ld_x(a.X + (size_t)(unsigned)cc[u] * xs + cx);  // unpredicated: dead steps are not added
+    }
+    load(p + U * W);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (p + u * W < f) acc = mul_add_rn(acc, vc[u], xv[u]);
+  }
+  sacc[t] = acc;
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll 1
+    for (int len = W; len > 1; len >>= 1)
+#pragma unroll 1
+      for (int i = 0; i < len / 2; ++i)
+        sacc[i * CW + cl] = __fadd_rn(sacc[(2 * i + 1) * CW + cl], sacc[2 * i * CW + cl]);
+    if (cok) a.Y[(size_t)(unsigned)a.rid[r] * xs + c] = sacc[cl];
+  }
+}
+
+}  // namespace spmk_dev

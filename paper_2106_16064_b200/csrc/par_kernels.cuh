@@ -36,6 +36,7 @@ struct ParArgs {
   int ncol_tile;      // columns per blockIdx.y pass
   long long TS;       // par-ws tile (T chunks of W)
   int nunits;
+  int hub;            // par-rs: rows with >= hub nonzeros belong to par_rs_hub_kernel
 };
 
 template <int W, int VL, int CT, bool VEC4>
@@ -136,6 +137,7 @@ par_rs_kernel(const ParArgs a) {
   first_batch(s1, f1, c1, w1);
   for (int r = gid; r < a.mne; r += groups_total) {
     const int s = s0, f = f0;
+    if (f - s < a.hub) {
     float acc[CT];
 #pragma unroll
     for (int k = 0; k < CT; ++k) acc[k] = 0.f;
@@ -205,6 +207,7 @@ par_rs_kernel(const ParArgs a) {
 #pragma unroll
       for (int i = 0; i < REM; ++i)
         if (cbase + i < nt) st_y(yr + cbase + i, acc[i]);
+    }
     }
     s0 = s1; f0 = f1; s1 = s2; f1 = f2;
 #pragma unroll

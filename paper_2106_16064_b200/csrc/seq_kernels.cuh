@@ -54,7 +54,6 @@ struct SeqArgs {
   long long TS;                  // ws: tile size in nnz (= T * CH)
   long long CH;                  // ws: chunk size (seq_chunk)
   long long EXT;                 // ws: owner-extension limit (row_is_long)
-  int RB;                        // rs: rows per tile
   int nunits;                    // tiles
   int cvvec;                     // colIdx/val 16-byte aligned (vector batch loads)
 };

@@ -20,6 +20,7 @@
 #include "../../include/spmk_capi.h"
 #include "aux_kernels.cuh"
 #include "gen_kernels.cuh"
+#include "hub_kernels.cuh"
 #include "iter_kernels.cuh"
 #include "par_kernels.cuh"
 #include "seq_kernels.cuh"
@@ -69,6 +70,7 @@ struct Plan {
   long long TS = 0, CH = 0, EXT = 0;
   int* longrows = nullptr;
   int nlong = 0;
+  std::vector<int> hrows;  // hub plans: hub rows in ascending order (host copy)
 };
 
 std::atomic<uint64_t> g_launches{0};
@@ -137,6 +139,12 @@ struct spmk_csr_s {
   // side stream for work that overlaps the variant kernels (empty-row fill)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // calls on different streams share the handle's scratch (long-row partial
+  // slots) and side stream: a call waits for the previous call's kernels when
+  // it comes on another stream (copies around the call still overlap)
+  cudaEvent_t ev_last = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
   std::mutex mu;
 };
 
@@ -162,6 +170,7 @@ void free_handle(spmk_csr_s* h) {
     cudaEventDestroy(h->ev_fork);
     cudaEventDestroy(h->ev_join);
   }
+  if (h->ev_last) cudaEventDestroy(h->ev_last);
   for (int i = 0; i < spmk_csr_s::kStageSlots; ++i) {
     cudaFree(h->stage_x[i]);
     cudaFree(h->stage_y[i]);
@@ -237,17 +246,97 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EX
   return h->plans.emplace(key, p).first->second;
 }
 
-// Row-split tile descriptors (RB compact rows per tile), cached like a plan.
-int4* get_rs_desc(spmk_csr_s* h, int RB, cudaStream_t s) {
-  auto key = std::make_tuple(3, (long long)RB, 0LL, 0LL);
+// Hub rows of the row-split variants (rows with >= L nonzeros, hub_kernels.cuh):
+// device list longest first (launch order), host copy ascending.
+Plan& get_hub_plan(spmk_csr_s* h, int L, cudaStream_t s) {
+  auto key = std::make_tuple(4, (long long)L, 0LL, 0LL);
   auto it = h->plans.find(key);
-  if (it != h->plans.end()) return it->second.desc;
+  if (it != h->plans.end()) return it->second;
   Plan p;
-  p.ntiles = (h->mne + RB - 1) / RB;
-  p.desc = dev_alloc<int4>((size_t)p.ntiles);
-  rs_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, h->mne, RB, p.ntiles, p.desc); LAUNCHED(1);
+  const long long cap = h->nnz / L + 1;
+  int2* list = dev_alloc<int2>((size_t)cap);
+  int* cnt = dev_alloc<int>(1);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+  hub_rows_kernel<<<grid_for(h->mne), 256, 0, s>>>(h->crp, h->mne, L, list, cnt); LAUNCHED(1);
   CK(cudaGetLastError());
-  return h->plans.emplace(key, p).first->second.desc;
+  int n = 0;
+  CK(cudaMemcpyAsync(&n, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (n > 0) {
+    std::vector<int2> hl((size_t)n);
+    CK(cudaMemcpyAsync(hl.data(), list, sizeof(int2) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::sort(hl.begin(), hl.end(), [](int2 x, int2 y) { return x.y != y.y ? x.y > y.y : x.x < y.x; });
+    std::vector<int> rows((size_t)n);
+    for (int i = 0; i < n; ++i) rows[i] = hl[i].x;
+    p.longrows = dev_alloc<int>((size_t)n);
+    CK(cudaMemcpyAsync(p.longrows, rows.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    std::sort(rows.begin(), rows.end());
+    p.hrows = std::move(rows);
+    CK(cudaStreamSynchronize(s));
+  }
+  p.nlong = n;
+  cudaFree(list);
+  cudaFree(cnt);
+  return h->plans.emplace(key, p).first->second;
+}
+
+// Row-split tile descriptors, cached like a plan: tile t holds the whole rows
+// that start in [t*TS, (t+1)*TS) (rlo of tile_plan_kernel), so tiles are
+// nnz-balanced without ever splitting a row (the row-split contract).  With
+// hub rows (hub plan `hub`), a tile holding hubs is cut into the runs of
+// non-hub rows between them: the first run keeps the tile's slot, the others
+// are appended; hub rows belong to no tile.
+Plan& get_rs_desc(spmk_csr_s* h, long long TS, int L, const Plan* hub, cudaStream_t s) {
+  auto key = std::make_tuple(3, TS, (long long)L, 0LL);
+  auto it = h->plans.find(key);
+  if (it != h->plans.end()) return it->second;
+  Plan p;
+  p.TS = TS;
+  p.ntiles = (h->nnz + TS - 1) / TS;
+  p.rlo = dev_alloc<int>((size_t)p.ntiles + 1);
+  tile_plan_kernel<<<grid_for(p.ntiles + 1), 256, 0, s>>>(h->crp, h->mne, p.ntiles, TS, p.rlo); LAUNCHED(1);
+  p.desc = dev_alloc<int4>((size_t)p.ntiles);
+  rs_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, p.rlo, p.ntiles, p.desc); LAUNCHED(1);
+  CK(cudaGetLastError());
+  if (hub && !hub->hrows.empty()) {
+    const std::vector<int>& hr = hub->hrows;
+    std::vector<int> rlo((size_t)p.ntiles + 1);
+    CK(cudaMemcpyAsync(rlo.data(), p.rlo, sizeof(int) * rlo.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<int4> extra;
+    std::vector<int> rp;
+    for (size_t i = 0; i < hr.size();) {
+      // the tile whose rows [rlo[t], rlo[t+1]) contain hub row hr[i]
+      const long long t = (long long)(std::upper_bound(rlo.begin(), rlo.end(), hr[i]) - rlo.begin()) - 1;
+      const int r0 = rlo[t], r1 = rlo[t + 1];
+      rp.resize((size_t)(r1 - r0) + 1);
+      CK(cudaMemcpyAsync(rp.data(), h->crp + r0, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::vector<int4> pieces;
+      int a0 = r0;
+      for (; i < hr.size() && hr[i] < r1; ++i) {
+        if (hr[i] > a0) pieces.push_back(make_int4(a0, rp[a0 - r0], rp[hr[i] - r0], MODE_NORMAL));
+        a0 = hr[i] + 1;
+      }
+      if (a0 < r1) pieces.push_back(make_int4(a0, rp[a0 - r0], rp[r1 - r0], MODE_NORMAL));
+      // an empty first run keeps the slot as an idle tile (start == end)
+      const int4 first = pieces.empty() ? make_int4(r0, 0, 0, MODE_NORMAL) : pieces[0];
+      CK(cudaMemcpyAsync(p.desc + t, &first, sizeof(int4), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      for (size_t k = 1; k < pieces.size(); ++k) extra.push_back(pieces[k]);
+    }
+    if (!extra.empty()) {
+      int4* d = dev_alloc<int4>((size_t)(p.ntiles + extra.size()));
+      CK(cudaMemcpyAsync(d, p.desc, sizeof(int4) * p.ntiles, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(d + p.ntiles, extra.data(), sizeof(int4) * extra.size(), cudaMemcpyHostToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      cudaFree(p.desc);
+      p.desc = d;
+      p.ntiles += (long long)extra.size();
+    }
+  }
+  return h->plans.emplace(key, p).first->second;
 }
 
 float* get_scratch(spmk_csr_s* h, size_t floats) {
@@ -289,6 +378,41 @@ bool need_smem_attr(const void* fn) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_attr_mu);
   return !std::exchange(g_attr_done[{fn, dev}], true);
+}
+
+// Hub threshold of the row-split variants (0 disables the hub path).
+int hub_threshold() { return (int)std::max(0LL, std::min<long long>(env_ll("SPMK_HUB_NNZ", 1024), INT32_MAX)); }
+
+template <int CW>
+void launch_seq_hub(const HubArgs& g, int nhub, int N, cudaStream_t s) {
+  // SPMK_HUB_SMEM pads the shared-memory request (e.g. 120 KB: one hub CTA
+  // per SM); measured neutral at N = 32 and slower at N = 128, so off.
+  const int smem = (int)std::max<long long>(hub_smem_bytes<CW>(), env_ll("SPMK_HUB_SMEM", 0));
+  if (need_smem_attr(reinterpret_cast<const void*>(seq_rs_hub_kernel<CW>)))
+    CK(cudaFuncSetAttribute(seq_rs_hub_kernel<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  seq_rs_hub_kernel<CW><<<dim3((unsigned)nhub, (unsigned)((N + CW - 1) / CW)), kHubThreads, smem, s>>>(g); LAUNCHED(1);
+}
+
+void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, const float* d_x, int N, float* d_y,
+                 cudaStream_t s) {
+  HubArgs g{hub.longrows, h->crp, h->rid, h->col, h->val, d_x, d_y, N};
+  int cw = 1;
+  while (cw < N && cw < 32) cw *= 2;  // columns per CTA
+  if (id == SPMK_SEQ_ROWSPLIT) {
+    switch (cw) {
+      case 1: launch_seq_hub<1>(g, hub.nlong, N, s); break;
+      case 2: launch_seq_hub<2>(g, hub.nlong, N, s); break;
+      case 4: launch_seq_hub<4>(g, hub.nlong, N, s); break;
+      case 8: launch_seq_hub<8>(g, hub.nlong, N, s); break;
+      case 16: launch_seq_hub<16>(g, hub.nlong, N, s); break;
+      default: launch_seq_hub<32>(g, hub.nlong, N, s); break;
+    }
+  } else {
+    cw = std::min(cw, kHubThreads / W);
+    const dim3 grid((unsigned)hub.nlong, (unsigned)((N + cw - 1) / cw));
+    par_rs_hub_kernel<<<grid, W * cw, 0, s>>>(g, W, cw); LAUNCHED(1);
+  }
+  CK(cudaGetLastError());
 }
 
 // ------------------------------------------------------------ seq launch
@@ -504,6 +628,10 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   if (n > INT32_MAX / 2) return fail(SPMK_EUNSUPPORTED, "n too large");
   if (id == SPMK_PAR_BALANCED && cfg.lane_width > 32)
     return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (!capturing && h->has_last && h->last_stream != s) CK(cudaStreamWaitEvent(s, h->ev_last, 0));
   timing_record(0, s);
   const int N = (int)n;
   const bool aligned = ((uintptr_t)d_x % 16 == 0) && ((uintptr_t)d_y % 16 == 0);
@@ -511,7 +639,13 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // kernels never touch empty rows, so the zero fill runs on the handle's
   // side stream concurrently with them (fork/join through events: HBM writes
   // overlap the gather-bound sweep; capturable into CUDA graphs).
-  const bool fork = h->nempty > 0;
+  // Row-split variants: hub rows (>= L nonzeros) run in hub_kernels.cuh on
+  // the side stream, concurrently with the main kernel (disjoint rows of Y).
+  const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
+  const int L = rs ? hub_threshold() : 0;
+  const Plan* hub = L > 0 ? &get_hub_plan(h, L, s) : nullptr;
+  const bool hubs = hub && hub->nlong > 0;
+  const bool fork = h->nempty > 0 || hubs;
   if (fork) {
     if (!h->side) {
       CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -520,7 +654,9 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     }
     CK(cudaEventRecord(h->ev_fork, s));
     CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    if (aligned && N % 4 == 0) {
+    if (hubs) launch_hubs(h, *hub, id, (int)cfg.lane_width, d_x, N, d_y, h->side);
+    if (h->nempty == 0) {
+    } else if (aligned && N % 4 == 0) {
       zero_rows_kernel<4><<<grid_for((long long)h->nempty * N / 4), 256, 0, h->side>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
     } else {
       zero_rows_kernel<1><<<grid_for((long long)h->nempty * N), 256, 0, h->side>>>(h->erow, h->nempty, N, d_y); LAUNCHED(1);
@@ -541,11 +677,10 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     a.cvvec = ((uintptr_t)h->col % 16 == 0) && ((uintptr_t)h->val % 16 == 0);
     if (id == SPMK_SEQ_ROWSPLIT) {
-      const double avg = (double)h->nnz / (double)h->mne;
-      int rb = (int)std::lround((double)env_ll("SPMK_SEQ_TILE_NNZ", 256) / std::max(avg, 1.0));
-      a.RB = std::max(1, std::min(rb, 256));
-      a.nunits = (h->mne + a.RB - 1) / a.RB;
-      a.desc = get_rs_desc(h, a.RB, s);
+      const long long TS = std::max(1LL, env_ll("SPMK_SEQ_TILE_NNZ", 256));
+      Plan& p = get_rs_desc(h, TS, L, hubs ? hub : nullptr, s);
+      a.nunits = (int)p.ntiles;
+      a.desc = p.desc;
       timing_record(1, s);
       launch_seq<false>(a, aligned, s);
       timing_record(2, s);
@@ -585,6 +720,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     const int W = (int)cfg.lane_width;
     if (id == SPMK_PAR_ROWSPLIT) {
+      a.hub = hubs ? L : INT32_MAX;
       timing_record(1, s);
       launch_par_rs(a, W, aligned, s);
       timing_record(2, s);
@@ -613,6 +749,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   if (fork) CK(cudaStreamWaitEvent(s, h->ev_join, 0));
   CK(cudaGetLastError());
   timing_record(3, s);
+  if (!capturing) {
+    if (!h->ev_last) CK(cudaEventCreateWithFlags(&h->ev_last, cudaEventDisableTiming));
+    CK(cudaEventRecord(h->ev_last, s));
+    h->last_stream = s;
+    h->has_last = true;
+  }
   return SPMK_OK;
 }
 

@@ -1,0 +1,118 @@
+"""Hub rows of the row-split variants (hub_kernels.cuh): rows with >= L
+nonzeros are skipped by the main par-rs / seq-rs kernels and computed by the
+hub kernels on the side stream, in the reference's order (kernels.hpp:157-224
+per-lane chains + tree; kernels.hpp:339-376 one ordered chain).  Bit-exact
+against the oracle for every lane width, column counts that are not multiples
+of the 32-column tile, and the tile-splitting edge cases (hub rows first,
+last, adjacent, filling a whole row-split tile, next to empty rows).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2106_16064_b200 as spmk  # noqa: E402
+from paper_2106_16064_b200.inputs import SKEWS  # noqa: E402
+from oracle.oracle import Csr  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def to_host(a: Csr):
+    return spmk.CsrMatrix(a.m, a.k, a.row_ptr, a.col_idx, a.val)
+
+
+def run(dev, kid, x_np, **cfg):
+    xd = torch.from_numpy(np.ascontiguousarray(x_np)).cuda()
+    y = dev.spmm(kid, xd, cfg=spmk.KernelConfig(**cfg) if cfg else None)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def assert_bits(y, want, ctx):
+    if not np.array_equal(y.view(np.uint32), want.view(np.uint32)):
+        bad = np.argwhere(y.view(np.uint32) != want.view(np.uint32))
+        i = tuple(bad[0])
+        raise AssertionError(f"{ctx}: {len(bad)} elements differ, first {i}: got {y[i]!r} want {want[i]!r}")
+
+
+def hub_matrix(orc, seed=5):
+    """Rows 0, 1 (adjacent), 40..47 (whole seq-rs tiles), 90 and
+    the last row are hubs; rows 2, 60 and 91 are empty."""
+    rng = np.random.default_rng(seed)
+    m, k = 128, 3000
+    lens = rng.integers(1, 12, m)
+    for r in (0, 1, *range(40, 48), 90, m - 1):
+        lens[r] = rng.integers(200, 2500)
+    for r in (2, 60, 91):
+        lens[r] = 0
+    rows, cols = [], []
+    for r in range(m):
+        c = rng.choice(k, size=lens[r], replace=False)
+        rows += [r] * len(c)
+        cols += list(c)
+    vals = rng.standard_normal(len(rows)).astype(np.float32)
+    a = orc.csr_from_coo(m, k, np.array(rows), np.array(cols), vals)
+    a.name = "hubs"
+    return a
+
+
+@pytest.fixture(scope="module")
+def cases(orc, corpus):
+    sel = [a for a in corpus if a.max_row_nnz() >= 16][:4] + [hub_matrix(orc)]
+    return [(a, spmk.DeviceCsr.from_host(to_host(a))) for a in sel]
+
+
+@pytest.mark.parametrize("L", [16, 100, 1000])
+def test_seq_rs_hub_rows_bit_exact(orc, cases, L, monkeypatch):
+    monkeypatch.setenv("SPMK_HUB_NNZ", str(L))
+    for a, d in cases:
+        for n in (1, 3, 32, 33, 64, 100):
+            x = orc.make_dense(a.k, n, 17 * n + L)
+            assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n} L={L}")
+
+
+@pytest.mark.parametrize("W", [2, 4, 8, 16, 32, 64])
+def test_par_rs_hub_rows_bit_exact(orc, cases, W, monkeypatch):
+    for L in (16, 300):
+        monkeypatch.setenv("SPMK_HUB_NNZ", str(L))
+        for a, d in cases:
+            for n in (1, 5, 32, 40):
+                x = orc.make_dense(a.k, n, 13 * n + W + L)
+                y = run(d, spmk.kParRowSplit, x, lane_width=W)
+                assert_bits(y, orc.spmm(a, 0, x, lane_width=W), f"{a.name} n={n} W={W} L={L}")
+
+
+def test_hub_rows_seq_rs_tile_sizes(orc, cases, monkeypatch):
+    """Different row-split tile sizes (rows per tile) cut differently around hubs."""
+    monkeypatch.setenv("SPMK_HUB_NNZ", "150")
+    a, d = cases[-1]
+    x = orc.make_dense(a.k, 8, 3)
+    want = orc.spmm(a, 2, x)
+    for tile in (16, 64, 256, 4096):
+        monkeypatch.setenv("SPMK_SEQ_TILE_NNZ", str(tile))
+        assert_bits(run(d, spmk.kSeqRowSplit, x), want, f"tile={tile}")
+
+
+def test_hub_path_disabled_matches(orc, cases, monkeypatch):
+    a, d = cases[-1]
+    x = orc.make_dense(a.k, 32, 9)
+    monkeypatch.setenv("SPMK_HUB_NNZ", "0")
+    y0 = run(d, spmk.kSeqRowSplit, x)
+    monkeypatch.setenv("SPMK_HUB_NNZ", "64")
+    y1 = run(d, spmk.kSeqRowSplit, x)
+    assert_bits(y1, y0, "seq-rs hub on/off")
+    assert_bits(y1, orc.spmm(a, 2, x), "seq-rs vs oracle")
+
+
+def test_hub_rows_rmat_heavy(orc, monkeypatch):
+    """Default threshold on a device R-MAT heavy graph (rows up to ~4K nonzeros)."""
+    monkeypatch.delenv("SPMK_HUB_NNZ", raising=False)
+    d = spmk.DeviceCsr.generate_rmat(16, 16, SKEWS["heavy"], 1)
+    h = d.download()
+    a = Csr(h.num_rows, h.num_cols, np.asarray(h.row_ptr), np.asarray(h.col_idx), np.asarray(h.values), "rmat16")
+    assert a.max_row_nnz() >= 1024
+    for n in (1, 32):
+        x = orc.make_dense(a.k, n, n)
+        assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"seq-rs n={n}")
+        assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), f"par-rs n={n}")
