@@ -71,6 +71,15 @@ struct Plan {
   int* longrows = nullptr;
   int nlong = 0;
   std::vector<int> hrows;  // hub plans: hub rows in ascending order (host copy)
+  std::vector<int> hlen;   // hub plans: hub row lengths in launch order
+};
+
+// Products-buffer layout of the hub rows for one N (par-rs two-pass path).
+struct HubLayout {
+  long long* po = nullptr;  // per hub: offset in floats (multiple of 4)
+  int2* segs = nullptr;     // per products block: {hub, first position}
+  int nsegs = 0;
+  long long floats = 0;     // buffer size (+ 16-byte slack)
 };
 
 std::atomic<uint64_t> g_launches{0};
@@ -128,6 +137,9 @@ struct spmk_csr_s {
   std::map<std::tuple<int, long long, long long, long long>, Plan> plans;
   float* scratch = nullptr;
   size_t scratch_floats = 0;
+  std::map<std::pair<int, int>, HubLayout> hub_layouts;  // (L, N)
+  float* hub_prod = nullptr;
+  size_t hub_prod_floats = 0;
   // host-operand staging: kStageSlots rotating (X, Y) device buffer pairs;
   // slot_done[i] marks the end of the last call that used slot i
   static constexpr int kStageSlots = 2;
@@ -164,6 +176,11 @@ void free_handle(spmk_csr_s* h) {
     cudaFree(kv.second.longrows);
   }
   cudaFree(h->scratch);
+  for (auto& kv : h->hub_layouts) {
+    cudaFree(kv.second.po);
+    cudaFree(kv.second.segs);
+  }
+  cudaFree(h->hub_prod);
   if (h->side) {
     cudaStreamSynchronize(h->side);
     cudaStreamDestroy(h->side);
@@ -269,6 +286,8 @@ Plan& get_hub_plan(spmk_csr_s* h, int L, cudaStream_t s) {
     std::sort(hl.begin(), hl.end(), [](int2 x, int2 y) { return x.y != y.y ? x.y > y.y : x.x < y.x; });
     std::vector<int> rows((size_t)n);
     for (int i = 0; i < n; ++i) rows[i] = hl[i].x;
+    p.hlen.resize((size_t)n);
+    for (int i = 0; i < n; ++i) p.hlen[i] = hl[i].y;
     p.longrows = dev_alloc<int>((size_t)n);
     CK(cudaMemcpyAsync(p.longrows, rows.data(), sizeof(int) * n, cudaMemcpyHostToDevice, s));
     std::sort(rows.begin(), rows.end());
@@ -393,9 +412,50 @@ void launch_seq_hub(const HubArgs& g, int nhub, int N, cudaStream_t s) {
   seq_rs_hub_kernel<CW><<<dim3((unsigned)nhub, (unsigned)((N + CW - 1) / CW)), kHubThreads, smem, s>>>(g); LAUNCHED(1);
 }
 
+const HubLayout& get_hub_layout(spmk_csr_s* h, const Plan& hub, int L, int N, cudaStream_t s) {
+  auto key = std::make_pair(L, N);
+  auto it = h->hub_layouts.find(key);
+  if (it != h->hub_layouts.end()) return it->second;
+  HubLayout lay;
+  std::vector<long long> po(hub.hlen.size());
+  std::vector<int2> segs;
+  long long off = 0;
+  for (size_t i = 0; i < hub.hlen.size(); ++i) {
+    po[i] = off;
+    off += ((long long)hub.hlen[i] * N + 3) / 4 * 4;
+    for (int q = 0; q < hub.hlen[i]; q += kHubSeg) segs.push_back(make_int2((int)i, q));
+  }
+  lay.floats = off + 4;
+  lay.nsegs = (int)segs.size();
+  lay.po = dev_alloc<long long>(po.size());
+  lay.segs = dev_alloc<int2>(segs.size());
+  CK(cudaMemcpyAsync(lay.po, po.data(), sizeof(long long) * po.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(lay.segs, segs.data(), sizeof(int2) * segs.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return h->hub_layouts.emplace(key, lay).first->second;
+}
+
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, const float* d_x, int N, float* d_y,
                  cudaStream_t s) {
   HubArgs g{hub.longrows, h->crp, h->rid, h->col, h->val, d_x, d_y, N};
+  if (id == SPMK_PAR_ROWSPLIT && W * N <= kHubThreads && env_ll("SPMK_HUB_TWO_PASS", 1)) {
+    const HubLayout& lay = get_hub_layout(h, hub, hub_threshold(), N, s);
+    if ((size_t)lay.floats > h->hub_prod_floats) {
+      cudaFree(h->hub_prod);
+      h->hub_prod = nullptr;
+      h->hub_prod_floats = 0;
+      h->hub_prod = dev_alloc<float>((size_t)lay.floats);
+      h->hub_prod_floats = (size_t)lay.floats;
+    }
+    HubProdArgs pa{hub.longrows, lay.segs, lay.po, h->crp, h->col, h->val, d_x, h->hub_prod, N};
+    hub_products_kernel<<<lay.nsegs, 256, 0, s>>>(pa); LAUNCHED(1);
+    constexpr int smem = 128 + kFoldStages * kFoldStageBytes;
+    if (need_smem_attr(reinterpret_cast<const void*>(par_rs_hub_fold_kernel)))
+      CK(cudaFuncSetAttribute(par_rs_hub_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    par_rs_hub_fold_kernel<<<hub.nlong, W * N, smem, s>>>(pa, h->rid, d_y, W); LAUNCHED(1);
+    CK(cudaGetLastError());
+    return;
+  }
   int cw = 1;
   while (cw < N && cw < 32) cw *= 2;  // columns per CTA
   if (id == SPMK_SEQ_ROWSPLIT) {

@@ -116,3 +116,14 @@ def test_hub_rows_rmat_heavy(orc, monkeypatch):
         x = orc.make_dense(a.k, n, n)
         assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"seq-rs n={n}")
         assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), f"par-rs n={n}")
+
+
+@pytest.mark.parametrize("kidx", [0, 2])
+def test_hub_path_full_corpus(orc, corpus, kidx, monkeypatch):
+    """Every corpus matrix with almost every row on the hub path (L = 16)."""
+    monkeypatch.setenv("SPMK_HUB_NNZ", "16")
+    for a in corpus:
+        d = spmk.DeviceCsr.from_host(to_host(a))
+        for n in (1, 4, 32):
+            x = orc.make_dense(a.k, n, 5 * n + kidx)
+            assert_bits(run(d, spmk.KernelId(kidx), x), orc.spmm(a, kidx, x), f"{a.name} n={n} k={kidx}")
