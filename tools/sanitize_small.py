@@ -14,5 +14,11 @@ for skew in ((0.57, 0.19, 0.19, 0.05), (0.25, 0.25, 0.25, 0.25)):
         for kid in spmk.kAllKernels:
             for cfg in (None, spmk.KernelConfig(lane_width=8, seq_chunk=16)):
                 d.spmm(kid, x, cfg=cfg)
+                if kid in (spmk.kParRowSplit, spmk.kSeqRowSplit):  # hub-row kernels on most rows
+                    os.environ["SPMK_HUB_NNZ"] = "8"
+                    d.spmm(kid, x, cfg=cfg)
+                    os.environ["SPMK_HUB_TWO_PASS"] = "0"
+                    d.spmm(kid, x, cfg=cfg)
+                    del os.environ["SPMK_HUB_TWO_PASS"], os.environ["SPMK_HUB_NNZ"]
     torch.cuda.synchronize()
 print("sanitize run ok")
