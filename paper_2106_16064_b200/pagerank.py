@@ -60,7 +60,7 @@ class PageRank:
     to 1/outdeg(col) unless ``stochastic=False``)."""
 
     def __init__(self, a: DeviceCsr, alpha: float = 0.85, kernel: Optional[KernelId] = None,
-                 stochastic: bool = True, counts=None):
+                 stochastic: bool = True, counts=None, l2_persist_bytes: int = 0):
         import torch
 
         if a.num_rows != a.num_cols:
@@ -77,6 +77,9 @@ class PageRank:
         self.scratch = torch.empty(int(_lib().spmk_pagerank_scratch_doubles()), dtype=torch.float64, device="cuda")
         self.graph = None
         self.hist = None
+        # bytes of x (from its start: the hot low-index columns of R-MAT
+        # graphs) kept in L2 by an access-policy window on the captured stream
+        self.l2_persist_bytes = int(l2_persist_bytes)
 
     def reset(self, x0=None):
         if x0 is None:
@@ -111,6 +114,10 @@ class PageRank:
         self.x.copy_(saved)
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
+        if self.l2_persist_bytes > 0:
+            from .spmk import l2_persist_x
+
+            l2_persist_x(s, self.x, min(self.l2_persist_bytes, self.m * 4))
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             self.stream = s
