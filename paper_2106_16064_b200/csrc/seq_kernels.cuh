@@ -311,9 +311,6 @@ seq_kernel(const SeqArgs a) {
 __device__ __forceinline__ void cp_async16(unsigned smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
 }
-__device__ __forceinline__ void cp_async16_ca(unsigned smem, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() {
@@ -457,8 +454,7 @@ constexpr int seq_async2_smem_bytes() {
   return NT * S * B * 16 + (NT / LPU) * 2 * SeqWin<LPU>::WIN * 4;
 }
 
-template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA = false, bool LATE = false,
-          bool UNR = true>
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT>
 __global__ void __launch_bounds__(NT, NT <= 64 ? 10 : NT <= 128 ? 5 : 1)
 seq_async2_kernel(const SeqArgs a) {
   static_assert((S & (S - 1)) == 0 && S >= 2, "S must be a power of two");
@@ -497,11 +493,7 @@ seq_async2_kernel(const SeqArgs a) {
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const unsigned cj = (unsigned)gshfl<LPU>(c[j / LPU], j % LPU);
-      if constexpr (CA) {
-        cp_async16_ca(ring0 + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)cj * xstride);
-      } else {
-        cp_async16(ring0 + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)cj * xstride);
-      }
+      cp_async16(ring0 + (unsigned)((stg * B + j) * NT * 16), xg + (size_t)cj * xstride);
     }
     cp_async_commit();
   };
@@ -509,7 +501,7 @@ seq_async2_kernel(const SeqArgs a) {
   int cring[S + 1][SLOTS];
   float vring[S + 1][SLOTS];
 #pragma unroll
-  for (int i = 0; i < (LATE ? S + 1 : S); ++i) load_cv(ea + i * B, cring[i], vring[i]);
+  for (int i = 0; i < S; ++i) load_cv(ea + i * B, cring[i], vring[i]);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s)
     if (ea + s * LPU + st.gl < st.e) vring[0][s] = 0.f;  // other rows before the unit start
@@ -521,7 +513,7 @@ seq_async2_kernel(const SeqArgs a) {
   int stage = 0;
 #pragma unroll 1
   for (int eb = ea; __any_sync(FULL, st.live); eb += B) {
-    if constexpr (!LATE) load_cv(eb + S * B, cring[S], vring[S]);
+    load_cv(eb + S * B, cring[S], vring[S]);  // refilled before the rotation (a refill after it: +15 %)
     issue((stage + S - 1) & (S - 1), cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     const float4* xs = ring + stage * B * NT + threadIdx.x;
@@ -547,44 +539,20 @@ seq_async2_kernel(const SeqArgs a) {
       return (st.live && d >= from && d < B) ? (1u << d) : 0u;
     };
     unsigned wm = __reduce_or_sync(FULL, next_bit(0));
-    if constexpr (UNR) {
-      // unrolled positions; a warp-uniform branch into the event handler
-      // only where some unit has an event (no repeated predicated passes):
-      // measured 9 % faster than the rounds form below (cfg2 320 -> 290 us)
+    // unrolled positions; a warp-uniform branch into the event handler only
+    // where some unit has an event (measured 9 % faster than add rounds
+    // between events: cfg2 320 -> 290 us)
 #pragma unroll
-      for (int j = 0; j < B; ++j) {
-        if (wm & (1u << j)) {
-          if (st.live && st.nev == eb + j) st.event(a, eb + j);
-          wm = __reduce_or_sync(FULL, next_bit(j + 1));
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          st.acc[k] = EXACT ? __fadd_rn(st.acc[k], px[j][k]) : fmaf(pv[j], px[j][k], st.acc[k]);
+    for (int j = 0; j < B; ++j) {
+      if (wm & (1u << j)) {
+        if (st.live && st.nev == eb + j) st.event(a, eb + j);
+        wm = __reduce_or_sync(FULL, next_bit(j + 1));
       }
-    } else {
-      int js = 0;
-#pragma unroll 1
-      while (true) {
-        const int je = wm ? (__ffs(wm) - 1) : B;
-        const unsigned rng = ((1u << je) - 1u) & ~((1u << js) - 1u);
 #pragma unroll
-        for (int j = 0; j < B; ++j) {
-          if ((rng >> j) & 1u) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              st.acc[k] = EXACT ? __fadd_rn(st.acc[k], px[j][k]) : fmaf(pv[j], px[j][k], st.acc[k]);
-          }
-        }
-        if (je >= B) break;
-        if (st.live && st.nev == eb + je) st.event(a, eb + je);
-        wm = __reduce_or_sync(FULL, next_bit(je + 1));
-        js = je;
-      }
+      for (int k = 0; k < 4; ++k)
+        st.acc[k] = EXACT ? __fadd_rn(st.acc[k], px[j][k]) : fmaf(pv[j], px[j][k], st.acc[k]);
     }
     stage = (stage + 1) & (S - 1);
-    // LATE: refill the top slot after the rotation (moves never wait on this
-    // iteration's loads) — measured 15 % slower on B200 than refilling at the
-    // top of the iteration (cfg2: 421 vs 358 us), so off by default.
 #pragma unroll
     for (int i = 0; i < S; ++i)
 #pragma unroll
@@ -592,7 +560,6 @@ seq_async2_kernel(const SeqArgs a) {
         cring[i][s] = cring[i + 1][s];
         vring[i][s] = vring[i + 1][s];
       }
-    if constexpr (LATE) load_cv(eb + (S + 1) * B, cring[S], vring[S]);
   }
   cp_async_wait<0>();
 }

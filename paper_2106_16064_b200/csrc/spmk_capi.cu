@@ -528,26 +528,26 @@ void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   else launch_seq_async_nt<WS, B, S, 256>(a, lpu, tiles, s);
 }
 
-template <int LPU, int B, int S, bool WS, int NT, bool EXACT, bool CA, bool LATE = false, bool UNR = true>
+template <int LPU, int B, int S, bool WS, int NT, bool EXACT>
 void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   constexpr int smem = seq_async2_smem_bytes<LPU, B, S, NT>();
-  if (need_smem_attr(reinterpret_cast<const void*>(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR>)))
-    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR>,
+  if (need_smem_attr(reinterpret_cast<const void*>(seq_async2_kernel<LPU, B, S, WS, NT, EXACT>)))
+    CK(cudaFuncSetAttribute(seq_async2_kernel<LPU, B, S, WS, NT, EXACT>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int upb = NT / LPU;
   dim3 grid((a.nunits + upb - 1) / upb, ncol_tiles);
-  seq_async2_kernel<LPU, B, S, WS, NT, EXACT, CA, LATE, UNR><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
+  seq_async2_kernel<LPU, B, S, WS, NT, EXACT><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
 }
 
-template <bool WS, int B, int S, int NT, bool EXACT, bool CA = false>
+template <bool WS, int B, int S, int NT, bool EXACT>
 void launch_seq_a2(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   switch (lpu) {
-    case 1: launch_seq_a2_t<1, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
-    case 2: launch_seq_a2_t<2, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
-    case 4: launch_seq_a2_t<4, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
-    case 8: launch_seq_a2_t<8, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
-    case 16: launch_seq_a2_t<16, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
-    default: launch_seq_a2_t<32, B, S, WS, NT, EXACT, CA>(a, tiles, s); break;
+    case 1: launch_seq_a2_t<1, B, S, WS, NT, EXACT>(a, tiles, s); break;
+    case 2: launch_seq_a2_t<2, B, S, WS, NT, EXACT>(a, tiles, s); break;
+    case 4: launch_seq_a2_t<4, B, S, WS, NT, EXACT>(a, tiles, s); break;
+    case 8: launch_seq_a2_t<8, B, S, WS, NT, EXACT>(a, tiles, s); break;
+    case 16: launch_seq_a2_t<16, B, S, WS, NT, EXACT>(a, tiles, s); break;
+    default: launch_seq_a2_t<32, B, S, WS, NT, EXACT>(a, tiles, s); break;
   }
 }
 
