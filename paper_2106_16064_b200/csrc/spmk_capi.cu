@@ -508,24 +508,14 @@ void launch_seq_async_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   seq_kernel_async<LPU, B, S, WS, NT><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
 }
 
+// N = 4..28 (1, 2 or 4 lanes per unit): the 3-stage ring, 128 threads
 template <bool WS, int B, int S, int NT>
-void launch_seq_async_nt(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
+void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   switch (lpu) {
     case 1: launch_seq_async_t<1, B, S, WS, NT>(a, tiles, s); break;
     case 2: launch_seq_async_t<2, B, S, WS, NT>(a, tiles, s); break;
-    case 4: launch_seq_async_t<4, B, S, WS, NT>(a, tiles, s); break;
-    case 8: launch_seq_async_t<8, B, S, WS, NT>(a, tiles, s); break;
-    case 16: launch_seq_async_t<16, B, S, WS, NT>(a, tiles, s); break;
-    default: launch_seq_async_t<32, B, S, WS, NT>(a, tiles, s); break;
+    default: launch_seq_async_t<4, B, S, WS, NT>(a, tiles, s); break;
   }
-}
-
-template <bool WS, int B, int S>
-void launch_seq_async(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
-  const long long nt = env_ll("SPMK_SEQ_NT", 128);
-  if (nt == 64) launch_seq_async_nt<WS, B, S, 64>(a, lpu, tiles, s);
-  else if (nt == 128) launch_seq_async_nt<WS, B, S, 128>(a, lpu, tiles, s);
-  else launch_seq_async_nt<WS, B, S, 256>(a, lpu, tiles, s);
 }
 
 template <int LPU, int B, int S, bool WS, int NT, bool EXACT>
@@ -539,12 +529,10 @@ void launch_seq_a2_t(const SeqArgs& a, int ncol_tiles, cudaStream_t s) {
   seq_async2_kernel<LPU, B, S, WS, NT, EXACT><<<grid, NT, smem, s>>>(a); LAUNCHED(1);
 }
 
+// N >= 32 (8, 16 or 32 lanes per unit): the 2-stage lean sweep
 template <bool WS, int B, int S, int NT, bool EXACT>
 void launch_seq_a2(const SeqArgs& a, int lpu, int tiles, cudaStream_t s) {
   switch (lpu) {
-    case 1: launch_seq_a2_t<1, B, S, WS, NT, EXACT>(a, tiles, s); break;
-    case 2: launch_seq_a2_t<2, B, S, WS, NT, EXACT>(a, tiles, s); break;
-    case 4: launch_seq_a2_t<4, B, S, WS, NT, EXACT>(a, tiles, s); break;
     case 8: launch_seq_a2_t<8, B, S, WS, NT, EXACT>(a, tiles, s); break;
     case 16: launch_seq_a2_t<16, B, S, WS, NT, EXACT>(a, tiles, s); break;
     default: launch_seq_a2_t<32, B, S, WS, NT, EXACT>(a, tiles, s); break;
@@ -560,14 +548,9 @@ void launch_seq(SeqArgs a, bool aligned, cudaStream_t s) {
     const int tiles = (N + a.ncol_tile - 1) / a.ncol_tile;
     // Measured on B200 (R-MAT s20 heavy/uniform, tools/probe_perf.py): the
     // lean 2-stage ring wins from 8 lanes per unit up (N >= 32), the 3-stage
-    // ring below.  Other variants stay selectable for experiments.
-    const long long variant = env_ll("SPMK_SEQ_VARIANT", lpu >= 8 ? 9 : 1);
-    if (variant == 0) launch_seq_lpu<WS, 4, true, 8>(a, lpu, tiles, s);
-    else if (variant == 2) launch_seq_async<WS, 4, 6>(a, lpu, tiles, s);
-    else if (variant == 9) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
-
-
-    else launch_seq_async<WS, 8, 3>(a, lpu, tiles, s);
+    // ring below (a register-pipelined sweep and a 6-stage ring were slower).
+    if (lpu >= 8) launch_seq_a2<WS, 8, 2, 128, true>(a, lpu, tiles, s);
+    else launch_seq_async<WS, 8, 3, 128>(a, lpu, tiles, s);
   } else if (aligned && N % 2 == 0 && N <= 64) {
     const int lpu = next_pow2(N / 2);
     a.ncol_tile = 2 * lpu;
