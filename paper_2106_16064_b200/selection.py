@@ -10,6 +10,9 @@ protocol (proj/include/spmk/bench.hpp) and threshold calibration
   min_single_kernel_loss     bench.hpp:198-202
   emit_csv                   bench.hpp:206-230
   calibrate_thresholds       selector.hpp:73-120
+  calibrate_thresholds_extended, holdout_calibration
+                             extension: n_parallel_max
+                             in the grid, held-out evaluation
 
 Device timing: `warmup` discarded calls, then `repeats` calls each bracketed by
 CUDA events on the launching stream, median taken (bench.hpp:74-92).  When
@@ -249,10 +252,7 @@ def _calibration_loss(cells, t: SelectorThresholds) -> float:
     return total / len(cells)
 
 
-def calibrate_thresholds(records: Sequence[CalibrationRecord]) -> SelectorThresholds:
-    """selector.hpp:73-120: grid search t_parallel_avg in {8..128} x t_cv in
-    {0.25..4} for the lowest mean loss; ties toward the defaults (log2
-    distance); n_parallel_max kept."""
+def _calibration_cells(records: Sequence[CalibrationRecord]):
     if not records:
         raise Error("calibrate_thresholds: empty record list")
     grouped: Dict[tuple, list] = {}
@@ -268,16 +268,59 @@ def calibrate_thresholds(records: Sequence[CalibrationRecord]) -> SelectorThresh
         if sum(1 for v in g if v >= 0.0) < 2:
             raise Error("calibration requires >= 2 kernels per (matrix, n) pair")
         cells.append((f, n, g))
+    return cells
+
+
+def _grid_search(cells, n_parallel_grid) -> SelectorThresholds:
     d = SelectorThresholds()
     best, best_loss, best_dist = d, _calibration_loss(cells, d), 0.0
-    for tp in (8.0, 16.0, 32.0, 64.0, 128.0):
-        for tc in (0.25, 0.5, 1.0, 2.0, 4.0):
-            cand = SelectorThresholds(d.n_parallel_max, tp, tc)
-            l = _calibration_loss(cells, cand)
-            dist = abs(math.log2(tp / d.t_parallel_avg)) + abs(math.log2(tc / d.t_cv))
-            if l < best_loss - 1e-12 or (l < best_loss + 1e-12 and dist < best_dist):
-                best, best_loss, best_dist = cand, l, dist
+    for npm in n_parallel_grid:
+        for tp in (8.0, 16.0, 32.0, 64.0, 128.0):
+            for tc in (0.25, 0.5, 1.0, 2.0, 4.0):
+                cand = SelectorThresholds(npm, tp, tc)
+                l = _calibration_loss(cells, cand)
+                dist = (abs(math.log2(npm / d.n_parallel_max)) + abs(math.log2(tp / d.t_parallel_avg))
+                        + abs(math.log2(tc / d.t_cv)))
+                if l < best_loss - 1e-12 or (l < best_loss + 1e-12 and dist < best_dist):
+                    best, best_loss, best_dist = cand, l, dist
     return best
+
+
+def calibrate_thresholds(records: Sequence[CalibrationRecord]) -> SelectorThresholds:
+    """selector.hpp:73-120: grid search t_parallel_avg in {8..128} x t_cv in
+    {0.25..4} for the lowest mean loss; ties toward the defaults (log2
+    distance); n_parallel_max kept."""
+    cells = _calibration_cells(records)
+    return _grid_search(cells, (SelectorThresholds().n_parallel_max,))
+
+
+def calibrate_thresholds_extended(records: Sequence[CalibrationRecord],
+                                  n_parallel_grid: Sequence[int] = (1, 2, 4, 8, 16, 32)) -> SelectorThresholds:
+    """Extension beyond the reference: the same grid and
+    tie rule as calibrate_thresholds, plus n_parallel_max over
+    `n_parallel_grid` (the N up to which the parallel-reduction variants are
+    chosen).  Ties still go toward the defaults, so a grid that cannot beat
+    them returns SelectorThresholds()."""
+    cells = _calibration_cells(records)
+    return _grid_search(cells, tuple(n_parallel_grid))
+
+
+def calibration_loss(records: Sequence[CalibrationRecord], t: SelectorThresholds) -> float:
+    """Mean selection loss of thresholds `t` over the (matrix, n) cells of
+    `records` (1 - chosen/best GFLOP/s, the calibration objective)."""
+    return _calibration_loss(_calibration_cells(records), t)
+
+
+def holdout_calibration(train: Sequence[CalibrationRecord], test: Sequence[CalibrationRecord],
+                        extended: bool = True) -> dict:
+    """Calibrate on `train`, report the loss on held-out `test` for the
+    default and the calibrated thresholds (a recalibrated
+    selector is reported on a held-out split)."""
+    cal = (calibrate_thresholds_extended if extended else calibrate_thresholds)(train)
+    d = SelectorThresholds()
+    return {"thresholds": cal.__dict__, "train_loss_default": calibration_loss(train, d),
+            "train_loss_calibrated": calibration_loss(train, cal), "test_loss_default": calibration_loss(test, d),
+            "test_loss_calibrated": calibration_loss(test, cal)}
 
 
 def calibration_records(records: Sequence[BenchRecord], features: Dict[str, MatrixFeatures]):

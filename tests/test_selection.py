@@ -140,3 +140,37 @@ def test_calibration_validation():  # test_selector.cpp:160-165
         sel.calibrate_thresholds([])
     with pytest.raises(spmk.Error):
         sel.calibrate_thresholds([sel.CalibrationRecord(feats(10, 1.0), 8, spmk.kSeqRowSplit, 1.0)])
+
+
+# ---- extension: n_parallel_max in the grid, held-out split
+def test_extended_calibration_keeps_defaults_when_they_are_optimal():
+    r = []
+    cal_cell(r, feats(50, 0.2), 32, [1, 1, 10, 2])
+    cal_cell(r, feats(5, 1.0), 2, [2, 10, 1, 1])
+    assert sel.calibrate_thresholds_extended(r) == spmk.SelectorThresholds()
+
+
+def test_extended_calibration_moves_the_parallel_crossover():
+    # parallel-reduction variants win up to N = 8 on these cells: the reference
+    # grid (n_parallel_max fixed at 4) cannot express that, the extension can
+    r = []
+    for i, n in enumerate((1, 2, 4, 8)):
+        cal_cell(r, feats(5 + i, 0.5), n, [1, 10, 2, 2])
+    for i, n in enumerate((16, 32, 64)):
+        cal_cell(r, feats(5 + i, 0.5), n, [1, 2, 10, 2])
+    base = sel.calibrate_thresholds(r)
+    ext = sel.calibrate_thresholds_extended(r)
+    assert base.n_parallel_max == 4
+    assert ext.n_parallel_max == 8
+    assert sel.calibration_loss(r, ext) == 0.0 < sel.calibration_loss(r, base)
+
+
+def test_holdout_calibration_reports_both_splits():
+    train, test = [], []
+    for i, n in enumerate((1, 2, 4, 8, 16)):
+        cal_cell(train, feats(5 + i, 0.5), n, [1, 10, 2, 2] if n <= 8 else [1, 2, 10, 2])
+        cal_cell(test, feats(6 + i, 0.6), n, [1, 10, 2, 2] if n <= 8 else [1, 2, 10, 2])
+    h = sel.holdout_calibration(train, test)
+    assert h["thresholds"]["n_parallel_max"] == 8
+    assert h["test_loss_calibrated"] == 0.0 < h["test_loss_default"]
+    assert h["train_loss_calibrated"] <= h["train_loss_default"]

@@ -47,13 +47,26 @@ def main():
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out + ".csv", "w") as f:
         selection.emit_csv(records, s, f)
-    cal = selection.calibrate_thresholds(selection.calibration_records(records, feats))
+    crecs = selection.calibration_records(records, feats)
+    cal = selection.calibrate_thresholds(crecs)
+    cal_ext = selection.calibrate_thresholds_extended(crecs)
+    # held-out split: calibrate on the even scales, evaluate on the odd ones
+    def scale_of(r):
+        return int(r.matrix_name.split("-s")[1].split("-")[0]) if "-s" in r.matrix_name else 0
+    train = selection.calibration_records([r for r in records if scale_of(r) % 2 == 0], feats)
+    test = selection.calibration_records([r for r in records if scale_of(r) % 2 == 1], feats)
+    holdout = selection.holdout_calibration(train, test) if train and test else None
     summary = {
         "per_n_loss": s.per_n_loss, "mean_per_n_loss": selection.mean_per_n_loss(s),
         "single_kernel_loss": s.single_kernel_loss,
         "min_single_kernel_loss": selection.min_single_kernel_loss(s),
         "all_correct": all(r.correct for r in records), "cells": len(records) // 5,
-        "calibrated_thresholds": cal.__dict__, "wall_s": round(time.time() - t0, 1),
+        "calibrated_thresholds": cal.__dict__,
+        "calibrated_thresholds_extended": cal_ext.__dict__,
+        "calibration_loss": {"default": selection.calibration_loss(crecs, selection.SelectorThresholds()),
+                             "calibrated": selection.calibration_loss(crecs, cal),
+                             "extended": selection.calibration_loss(crecs, cal_ext)},
+        "holdout_even_train_odd_test": holdout, "wall_s": round(time.time() - t0, 1),
     }
     with open(args.out + ".json", "w") as f:
         json.dump(summary, f, indent=1)
