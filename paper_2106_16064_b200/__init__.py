@@ -35,3 +35,4 @@ from .spmk import (  # noqa: F401
     select_kernel,
     spmm,
 )
+from .mmio import MatrixMarketHeader, csr_from_coo, read_matrix_market, write_matrix_market  # noqa: F401,E402

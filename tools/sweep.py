@@ -5,6 +5,7 @@ the rule, bench.hpp semantics (median of repeats, L2 flushed).  Writes the
 reference's CSV (emit_csv) and a JSON summary.
 
     python tools/sweep.py [--scales 18,20,22] [--ns 1,2,4,8,16,32,64,128] [--out profiles/r01_sweep]
+    python tools/sweep.py --mtx a.mtx,b.mtx      # real matrices (Matrix Market) instead
 """
 import argparse
 import json
@@ -14,6 +15,7 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import paper_2106_16064_b200 as spmk  # noqa: E402
 from paper_2106_16064_b200 import inputs, selection  # noqa: E402
 
 
@@ -26,12 +28,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--out", default="gpurun_out/sweep")
+    ap.add_argument("--mtx", default="", help="comma-separated Matrix Market files (replaces the synthetic corpus)")
     args = ap.parse_args()
     scales = [int(s) for s in args.scales.split(",")]
     ns = [int(n) for n in args.ns.split(",")]
     t0 = time.time()
     records, feats = [], {}
-    for name, a in inputs.sweep_corpus(scales, args.families.split(",")):
+    if args.mtx:
+        corpus = ((os.path.splitext(os.path.basename(p))[0], spmk.DeviceCsr.from_host(spmk.read_matrix_market(p)))
+                  for p in args.mtx.split(","))
+    else:
+        corpus = inputs.sweep_corpus(scales, args.families.split(","))
+    for name, a in corpus:
         feats[name] = a.features()
         print(f"{name}: rows {a.num_rows} nnz {a.nnz} avg {feats[name].avg_row:.2f} cv {feats[name].cv:.3f}",
               flush=True)
