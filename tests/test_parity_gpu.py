@@ -252,8 +252,10 @@ def test_row_slices_parity(orc):
 @pytest.mark.slow
 def test_cfg2_full_size(orc):
     """BASELINE cfg2 at full size: R-MAT s20 e16 heavy seed 1, N=32.
-    Bit-exact vs the reference order for the rule's pick (seq-ws) and par-ws;
-    all four within the north_star bound on a row sample incl. the hub rows."""
+    All four variants bit-exact vs the reference order (the row-split ones
+    with their 1,351 hub rows on the hub path; par-rs also at N=1, where the
+    hub rows take the two-pass products + streamed-fold path) and within the
+    north_star bound on a row sample incl. the hub rows."""
     d = spmk.DeviceCsr.generate_rmat(20, 16, (0.57, 0.19, 0.19, 0.05), 1)
     assert d.nnz == 16083729
     assert d.select(32) == spmk.kSeqBalanced
@@ -270,5 +272,11 @@ def test_cfg2_full_size(orc):
         torch.cuda.synchronize()
         yh = y.cpu().numpy()
         assert_tol(yh[rows], y64, bound, f"cfg2 {kid.name}")
-        if kid in (spmk.kSeqBalanced, spmk.kParBalanced):
-            assert_bits(yh, orc.spmm(a, kid.index, xh), f"cfg2 {kid.name}")
+        assert_bits(yh, orc.spmm(a, kid.index, xh), f"cfg2 {kid.name}")
+    x1 = spmk.make_dense_device(a.k, 1, 0x00D5EED + 1)
+    torch.cuda.synchronize()
+    x1h = x1.cpu().numpy()
+    for kid in (spmk.kParRowSplit, spmk.kSeqRowSplit):
+        y = d.spmm(kid, x1)
+        torch.cuda.synchronize()
+        assert_bits(y.cpu().numpy(), orc.spmm(a, kid.index, x1h), f"cfg2 N=1 {kid.name}")
