@@ -127,3 +127,27 @@ def test_hub_path_full_corpus(orc, corpus, kidx, monkeypatch):
         for n in (1, 4, 32):
             x = orc.make_dense(a.k, n, 5 * n + kidx)
             assert_bits(run(d, spmk.KernelId(kidx), x), orc.spmm(a, kidx, x), f"{a.name} n={n} k={kidx}")
+
+
+@pytest.mark.slow
+def test_cfg5_hub_slice_bit_exact(orc):
+    """BASELINE cfg5 graph (R-MAT s25 e16 heavy seed 1), slice 0 of the 8-way
+    equal-nnz partition: 66M nonzeros, 51.7M of them in 11,104 hub rows (max
+    373,191), the slice the per-slice rule sends to par-rs at N=1.  The
+    two-pass hub path is bit-exact against the reference order."""
+    monkeypatch_env = pytest.MonkeyPatch()
+    monkeypatch_env.delenv("SPMK_HUB_NNZ", raising=False)
+    try:
+        full = spmk.DeviceCsr.generate_rmat(25, 16, SKEWS["heavy"], 1)
+        b = full.row_slices(8)
+        d = full.slice(int(b[0]), int(b[1]))
+        del full
+        torch.cuda.empty_cache()
+        assert d.select(1) == spmk.kParRowSplit
+        h = d.download()
+        a = Csr(h.num_rows, h.num_cols, np.asarray(h.row_ptr), np.asarray(h.col_idx), np.asarray(h.values), "cfg5s0")
+        assert a.max_row_nnz() == 373191
+        x = orc.make_dense(a.k, 1, 0x00D5EED + 1)
+        assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), "cfg5 slice 0 par-rs")
+    finally:
+        monkeypatch_env.undo()
