@@ -400,7 +400,13 @@ bool need_smem_attr(const void* fn) {
 }
 
 // Hub threshold of the row-split variants (0 disables the hub path).
-int hub_threshold() { return (int)std::max(0LL, std::min<long long>(env_ll("SPMK_HUB_NNZ", 1024), INT32_MAX)); }
+// Measured on B200 (R-MAT s20..s25 heavy): par-rs 2048 (s25 N=1: 3.91 ms at
+// 1024, 3.37 ms at 2048, 3.50 ms at 4096), seq-rs 1024 (s20 N=32: 0.77 ms,
+// 0.88 ms at 4096).
+int hub_threshold(spmk_kernel_id id) {
+  const long long dflt = id == SPMK_PAR_ROWSPLIT ? 2048 : 1024;
+  return (int)std::max(0LL, std::min<long long>(env_ll("SPMK_HUB_NNZ", dflt), INT32_MAX));
+}
 
 template <int CW>
 void launch_seq_hub(const HubArgs& g, int nhub, int N, cudaStream_t s) {
@@ -439,7 +445,7 @@ void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, const
                  cudaStream_t s) {
   HubArgs g{hub.longrows, h->crp, h->rid, h->col, h->val, d_x, d_y, N};
   if (id == SPMK_PAR_ROWSPLIT && W * N <= kHubThreads && env_ll("SPMK_HUB_TWO_PASS", 1)) {
-    const HubLayout& lay = get_hub_layout(h, hub, hub_threshold(), N, s);
+    const HubLayout& lay = get_hub_layout(h, hub, hub_threshold(id), N, s);
     if ((size_t)lay.floats > h->hub_prod_floats) {
       cudaFree(h->hub_prod);
       h->hub_prod = nullptr;
@@ -685,7 +691,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // Row-split variants: hub rows (>= L nonzeros) run in hub_kernels.cuh on
   // the side stream, concurrently with the main kernel (disjoint rows of Y).
   const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
-  const int L = rs ? hub_threshold() : 0;
+  const int L = rs ? hub_threshold(id) : 0;
   const Plan* hub = L > 0 ? &get_hub_plan(h, L, s) : nullptr;
   const bool hubs = hub && hub->nlong > 0;
   const bool fork = h->nempty > 0 || hubs;

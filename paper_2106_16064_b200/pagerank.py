@@ -59,7 +59,7 @@ class PageRank:
     """Single-GPU iterative SpMV on a resident, square A (values are rewritten
     to 1/outdeg(col) unless ``stochastic=False``)."""
 
-    def __init__(self, a: DeviceCsr, alpha: float = 0.85, kernel: Optional[KernelId] = None,
+    def __init__(self, a: DeviceCsr, alpha: float = 0.85, kernel=None,
                  stochastic: bool = True, counts=None, l2_persist_bytes: int = 0):
         import torch
 
@@ -70,7 +70,14 @@ class PageRank:
         self.counts = counts if counts is not None else column_counts(a, self.stream)
         if stochastic:
             make_column_stochastic(a, self.counts, self.stream)
-        self.kid = kernel if kernel is not None else a.select(1)
+        # kernel: a KernelId, None (the selection rule, select_kernel) or
+        # "tuned" (the fastest variant measured on this graph, selection.tuned_kernel)
+        if kernel == "tuned":
+            from .selection import tuned_kernel
+
+            self.kid, self.tune_times = tuned_kernel(a, 1)
+        else:
+            self.kid = kernel if kernel is not None else a.select(1)
         self.x = torch.full((self.m, 1), 1.0 / self.m, dtype=torch.float32, device="cuda")
         self.y = torch.empty((self.m, 1), dtype=torch.float32, device="cuda")
         self.state = torch.zeros(3, dtype=torch.float64, device="cuda")
@@ -183,7 +190,7 @@ class DistributedPageRank:
     update and all-gather fused into one kernel; the residual all-reduce that
     follows is the barrier before the next SpMV reads x_next."""
 
-    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None, exchange: str = "nccl"):
+    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None, exchange: str = "nccl", kernel=None):
         import torch
         import torch.distributed as dist
 
@@ -200,7 +207,14 @@ class DistributedPageRank:
         dist.all_reduce(counts, group=group)  # global out-degrees (integer: exact)
         self.counts = counts
         make_column_stochastic(self.a, counts)
-        self.kid = self.a.select(1)
+        # per-slice choice: the rule on this slice's features (None), "tuned"
+        # (fastest variant measured on this slice) or a fixed KernelId
+        if kernel == "tuned":
+            from .selection import tuned_kernel
+
+            self.kid, self.tune_times = tuned_kernel(self.a, 1)
+        else:
+            self.kid = kernel if kernel is not None else self.a.select(1)
         self.y = torch.empty((hi - lo, 1), dtype=torch.float32, device="cuda")
         self.state = torch.zeros(3, dtype=torch.float64, device="cuda")
         self.scratch = torch.empty(int(_lib().spmk_pagerank_scratch_doubles()), dtype=torch.float64, device="cuda")

@@ -10,6 +10,7 @@ protocol (proj/include/spmk/bench.hpp) and threshold calibration
   min_single_kernel_loss     bench.hpp:198-202
   emit_csv                   bench.hpp:206-230
   calibrate_thresholds       selector.hpp:73-120
+  tuned_kernel               empirical per-matrix selection (extension)
   calibrate_thresholds_extended, holdout_calibration
                              extension: n_parallel_max
                              in the grid, held-out evaluation
@@ -101,6 +102,26 @@ def measure_kernel(name: str, a: DeviceCsr, x, kid: KernelId, cfg=None, repeats:
     rec = BenchRecord(name, a.num_rows, a.num_cols, a.nnz, n, kernel_name(kid), t,
                       2.0 * a.nnz * n / t / 1e9)
     return rec, y
+
+
+def tuned_kernel(a: DeviceCsr, n: int, candidates: Sequence[KernelId] = kAllKernels, cfg=None,
+                 repeats: int = 3, warmup: int = 1) -> Tuple[KernelId, Dict[str, float]]:
+    """Empirical selection (the paper's per-input oracle, measured instead of
+    predicted): time every candidate variant on this matrix at width n with
+    measure_kernel and return the fastest with all times.  Every variant is
+    exact in its own reference order, so the choice changes speed and the
+    summation order, never the tolerance contract.  Used by iterative
+    drivers that amortise the tuning over many calls (pagerank.PageRank)."""
+    from .spmk import make_dense_device
+
+    x = make_dense_device(a.num_cols, n, 0x00D5EED + n)
+    times = {}
+    for kid in candidates:
+        rec, y = measure_kernel("tune", a, x, kid, cfg=cfg, repeats=repeats, warmup=warmup, flush_l2=False)
+        times[kid.name] = rec.time_seconds
+        del y
+    best = min(candidates, key=lambda k: times[k.name])
+    return best, times
 
 
 def _abs_matrix(a: DeviceCsr) -> DeviceCsr:

@@ -132,7 +132,7 @@ def test_hub_path_full_corpus(orc, corpus, kidx, monkeypatch):
 @pytest.mark.slow
 def test_cfg5_hub_slice_bit_exact(orc):
     """BASELINE cfg5 graph (R-MAT s25 e16 heavy seed 1), slice 0 of the 8-way
-    equal-nnz partition: 66M nonzeros, 51.7M of them in 11,104 hub rows (max
+    equal-nnz partition: 66M nonzeros, 51.7M of them in the 11,104 rows >= 1024 (max
     373,191), the slice the per-slice rule sends to par-rs at N=1.  The
     two-pass hub path is bit-exact against the reference order."""
     monkeypatch_env = pytest.MonkeyPatch()

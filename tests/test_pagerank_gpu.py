@@ -107,3 +107,15 @@ def test_graph_replay_row_split_hub_path(graph, kidx, monkeypatch):
     x_graph, h_graph = pr.run(10, graph=True)
     assert np.array_equal(x_graph.cpu().numpy(), x_eager)
     assert np.array_equal(h_graph.cpu().numpy(), h_eager)
+
+
+def test_tuned_kernel_choice(graph, orc):
+    """kernel="tuned": the fastest measured variant; any variant stays within
+    the north-star bound, so the free-running iteration keeps its contract."""
+    d, _, a, counts = graph
+    pr = prk.PageRank(d, ALPHA, kernel="tuned")
+    assert set(pr.tune_times) == {k.name for k in spmk.kAllKernels}
+    assert pr.tune_times[pr.kid.name] == min(pr.tune_times.values())
+    x, _ = pr.run(30, graph=True)
+    ref = pagerank64(orc, a, counts, ALPHA, 30)
+    assert np.abs(x.cpu().numpy().reshape(-1) - ref).sum() <= 1e-5 / (1 - ALPHA)

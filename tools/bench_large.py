@@ -23,6 +23,7 @@ ap.add_argument("--ef", type=int, default=32)
 ap.add_argument("--n", type=int, default=64)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--parts", default="2,4,8")
+ap.add_argument("--kernel", default="rule", help="rule (select_kernel per matrix / slice) or tuned (fastest measured)")
 args = ap.parse_args()
 t0 = time.time()
 full = spmk.DeviceCsr.generate_rmat(args.scale, args.ef, (0.57, 0.19, 0.19, 0.05), 1)
@@ -30,7 +31,11 @@ torch.cuda.synchronize()
 gen = time.time() - t0
 n = args.n
 x = spmk.make_dense_device(full.num_cols, n, 0x00D5EED + n)
-kid = full.select(n)
+def choose(a):
+    return selection.tuned_kernel(a, n)[0] if args.kernel == "tuned" else a.select(n)
+
+
+kid = choose(full)
 rec, y = selection.measure_kernel("cfg4", full, x, kid, repeats=args.reps, warmup=1)
 t1 = rec.time_seconds
 del y
@@ -39,7 +44,8 @@ M, K, nnz = full.num_rows, full.num_cols, full.nnz
 byts = 4 * (M + 1) + 8 * nnz + 4 * K * n + 4 * M * n
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"]
-out = {"workload": f"cfg4 SpMM N={n} on R-MAT s{args.scale} e{args.ef} heavy seed 1", "nnz": nnz,
+out = {"workload": f"SpMM N={n} on R-MAT s{args.scale} e{args.ef} heavy seed 1", "nnz": nnz,
+       "kernel_choice": args.kernel,
        "kernel": kid.name, "t1_ms": round(t1 * 1e3, 3), "gflops_1gpu": round(rec.gflops, 1),
        "roofline_frac_of_measured_hbm": round(byts / t1 / 1e9 / peak, 4), "generation_s": round(gen, 1),
        "partitions": {}}
@@ -48,7 +54,7 @@ for G in [int(g) for g in args.parts.split(",")]:
     ts, kinds = [], []
     for g in range(G):
         s = full.slice(int(b[g]), int(b[g + 1]))
-        k = s.select(n)
+        k = choose(s)
         r, yy = selection.measure_kernel(f"slice{g}", s, x, k, repeats=args.reps, warmup=1)
         ts.append(r.time_seconds)
         kinds.append(k.name)

@@ -21,12 +21,14 @@ ap.add_argument("--ef", type=int, default=16)
 ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--l2", type=float, default=0.0, help="MB of x (its hot low-index prefix) pinned in L2")
+ap.add_argument("--kernel", default="rule", help="rule | tuned | par-rs | par-ws | seq-rs | seq-ws")
 args = ap.parse_args()
 t0 = time.time()
 d = spmk.DeviceCsr.generate_rmat(args.scale, args.ef, (0.57, 0.19, 0.19, 0.05), 1)
 torch.cuda.synchronize()
 gen = time.time() - t0
-pr = prk.PageRank(d, 0.85, l2_persist_bytes=int(args.l2 * (1 << 20)))
+kern = None if args.kernel == "rule" else ("tuned" if args.kernel == "tuned" else spmk.parse_kernel(args.kernel))
+pr = prk.PageRank(d, 0.85, kernel=kern, l2_persist_bytes=int(args.l2 * (1 << 20)))
 pr.capture(args.iters)
 ts = []
 for _ in range(args.reps):
@@ -46,7 +48,7 @@ peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
 hist = pr.hist.cpu().numpy()
 print(json.dumps({
     "workload": f"cfg5 iterative SpMV (PageRank, alpha 0.85) on R-MAT s{args.scale} e{args.ef} heavy seed 1, 1 B200",
-    "nnz": nnz, "kernel": pr.kid.name, "l2_persist_MB": args.l2, "iters": args.iters, "ms_total": round(t * 1e3, 3),
+    "nnz": nnz, "kernel": pr.kid.name, "kernel_choice": args.kernel, "l2_persist_MB": args.l2, "iters": args.iters, "ms_total": round(t * 1e3, 3),
     "us_per_iter": round(per * 1e6, 1), "gflops": round(2.0 * nnz / per / 1e9, 1),
     "GBps_compulsory": round(byts / per / 1e9, 1), "roofline_frac_of_measured_hbm": round(byts / per / 1e9 / peak, 4),
     "l1_residual_first_last": [float(hist[0]), float(hist[-1])], "generation_s": round(gen, 1)}))
