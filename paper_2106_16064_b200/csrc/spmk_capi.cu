@@ -319,41 +319,37 @@ Plan& get_rs_desc(spmk_csr_s* h, long long TS, int L, const Plan* hub, cudaStrea
   rs_tile_desc_kernel<<<grid_for(p.ntiles), 256, 0, s>>>(h->crp, p.rlo, p.ntiles, p.desc); LAUNCHED(1);
   CK(cudaGetLastError());
   if (hub && !hub->hrows.empty()) {
+    // one round trip: row metadata and descriptors down, edited, back up
     const std::vector<int>& hr = hub->hrows;
-    std::vector<int> rlo((size_t)p.ntiles + 1);
+    std::vector<int> rlo((size_t)p.ntiles + 1), rp((size_t)h->mne + 1);
+    std::vector<int4> desc((size_t)p.ntiles);
     CK(cudaMemcpyAsync(rlo.data(), p.rlo, sizeof(int) * rlo.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rp.data(), h->crp, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(desc.data(), p.desc, sizeof(int4) * desc.size(), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    std::vector<int4> extra;
-    std::vector<int> rp;
     for (size_t i = 0; i < hr.size();) {
       // the tile whose rows [rlo[t], rlo[t+1]) contain hub row hr[i]
       const long long t = (long long)(std::upper_bound(rlo.begin(), rlo.end(), hr[i]) - rlo.begin()) - 1;
       const int r0 = rlo[t], r1 = rlo[t + 1];
-      rp.resize((size_t)(r1 - r0) + 1);
-      CK(cudaMemcpyAsync(rp.data(), h->crp + r0, sizeof(int) * rp.size(), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
       std::vector<int4> pieces;
       int a0 = r0;
       for (; i < hr.size() && hr[i] < r1; ++i) {
-        if (hr[i] > a0) pieces.push_back(make_int4(a0, rp[a0 - r0], rp[hr[i] - r0], MODE_NORMAL));
+        if (hr[i] > a0) pieces.push_back(make_int4(a0, rp[a0], rp[hr[i]], MODE_NORMAL));
         a0 = hr[i] + 1;
       }
-      if (a0 < r1) pieces.push_back(make_int4(a0, rp[a0 - r0], rp[r1 - r0], MODE_NORMAL));
+      if (a0 < r1) pieces.push_back(make_int4(a0, rp[a0], rp[r1], MODE_NORMAL));
       // an empty first run keeps the slot as an idle tile (start == end)
-      const int4 first = pieces.empty() ? make_int4(r0, 0, 0, MODE_NORMAL) : pieces[0];
-      CK(cudaMemcpyAsync(p.desc + t, &first, sizeof(int4), cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
-      for (size_t k = 1; k < pieces.size(); ++k) extra.push_back(pieces[k]);
+      desc[t] = pieces.empty() ? make_int4(r0, 0, 0, MODE_NORMAL) : pieces[0];
+      for (size_t k = 1; k < pieces.size(); ++k) desc.push_back(pieces[k]);
     }
-    if (!extra.empty()) {
-      int4* d = dev_alloc<int4>((size_t)(p.ntiles + extra.size()));
-      CK(cudaMemcpyAsync(d, p.desc, sizeof(int4) * p.ntiles, cudaMemcpyDeviceToDevice, s));
-      CK(cudaMemcpyAsync(d + p.ntiles, extra.data(), sizeof(int4) * extra.size(), cudaMemcpyHostToDevice, s));
-      CK(cudaStreamSynchronize(s));
+    if ((long long)desc.size() != p.ntiles) {
       cudaFree(p.desc);
-      p.desc = d;
-      p.ntiles += (long long)extra.size();
+      p.desc = nullptr;
+      p.desc = dev_alloc<int4>(desc.size());
+      p.ntiles = (long long)desc.size();
     }
+    CK(cudaMemcpyAsync(p.desc, desc.data(), sizeof(int4) * desc.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
   }
   return h->plans.emplace(key, p).first->second;
 }
