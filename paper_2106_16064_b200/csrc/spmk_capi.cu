@@ -440,7 +440,12 @@ const HubLayout& get_hub_layout(spmk_csr_s* h, const Plan& hub, int L, int N, cu
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, const float* d_x, int N, float* d_y,
                  cudaStream_t s) {
   HubArgs g{hub.longrows, h->crp, h->rid, h->col, h->val, d_x, d_y, N};
-  if (id == SPMK_PAR_ROWSPLIT && W * N <= kHubThreads && env_ll("SPMK_HUB_TWO_PASS", 1)) {
+  // seq-rs is the fold with one chain per column (W = 1: every position in
+  // order, no tree) — kernels.hpp:366-370
+  const bool seq = id == SPMK_SEQ_ROWSPLIT;
+  const int FW = seq ? 1 : W;
+  const long long two_pass = env_ll("SPMK_HUB_TWO_PASS", seq ? 0 : 1);
+  if (two_pass && FW * N <= kHubThreads) {
     const HubLayout& lay = get_hub_layout(h, hub, hub_threshold(id), N, s);
     if ((size_t)lay.floats > h->hub_prod_floats) {
       cudaFree(h->hub_prod);
@@ -454,7 +459,7 @@ void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, const
     constexpr int smem = 128 + kFoldStages * kFoldStageBytes;
     if (need_smem_attr(reinterpret_cast<const void*>(par_rs_hub_fold_kernel)))
       CK(cudaFuncSetAttribute(par_rs_hub_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    par_rs_hub_fold_kernel<<<hub.nlong, W * N, smem, s>>>(pa, h->rid, d_y, W); LAUNCHED(1);
+    par_rs_hub_fold_kernel<<<hub.nlong, FW * N, smem, s>>>(pa, h->rid, d_y, FW); LAUNCHED(1);
     CK(cudaGetLastError());
     return;
   }

@@ -151,3 +151,15 @@ def test_cfg5_hub_slice_bit_exact(orc):
         assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), "cfg5 slice 0 par-rs")
     finally:
         monkeypatch_env.undo()
+
+
+def test_seq_rs_two_pass_fold(orc, cases, monkeypatch):
+    """seq-rs through the products + streamed-fold path (one chain per column,
+    SPMK_HUB_TWO_PASS=1; off by default because the producer/folder kernel
+    is faster for seq-rs) gives the same bits."""
+    monkeypatch.setenv("SPMK_HUB_NNZ", "16")
+    monkeypatch.setenv("SPMK_HUB_TWO_PASS", "1")
+    for a, d in cases:
+        for n in (1, 3, 32, 100):
+            x = orc.make_dense(a.k, n, 11 * n)
+            assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n}")
