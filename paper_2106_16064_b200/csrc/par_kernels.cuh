@@ -100,25 +100,15 @@ par_rs_kernel(const ParArgs a) {
       }
     }
   };
-  // lane-sequential FMA chain (kernels.hpp:181-186); dead lanes add nothing
-  auto fma_batch = [&](const int (&c)[VL], const float (&w)[VL], const float (&xall)[VL][CT], float (&acc)[CT],
-                       float (&acc2)[VL == 2 ? CT : 1]) {
+  // lane-sequential FMA chain (kernels.hpp:181-186); dead lanes add nothing.
+  // Virtual lane gl*VL+v keeps its own chain acc[v].
+  auto fma_batch = [&](const int (&c)[VL], const float (&w)[VL], const float (&xall)[VL][CT],
+                       float (&acc)[VL][CT]) {
 #pragma unroll
     for (int v = 0; v < VL; ++v) {
       if (c[v] >= 0) {
-        const float (&xv)[CT] = xall[v];
-        if constexpr (VL == 2) {
-          if (v == 1) {
 #pragma unroll
-            for (int k = 0; k < CT; ++k) acc2[k] = mul_add_rn(acc2[k], w[v], xv[k]);
-          } else {
-#pragma unroll
-            for (int k = 0; k < CT; ++k) acc[k] = mul_add_rn(acc[k], w[v], xv[k]);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < CT; ++k) acc[k] = mul_add_rn(acc[k], w[v], xv[k]);
-        }
+        for (int k = 0; k < CT; ++k) acc[v][k] = mul_add_rn(acc[v][k], w[v], xall[v][k]);
       }
     }
   };
@@ -138,20 +128,21 @@ par_rs_kernel(const ParArgs a) {
   for (int r = gid; r < a.mne; r += groups_total) {
     const int s = s0, f = f0;
     if (f - s < a.hub) {
-    float acc[CT];
+    float accv[VL][CT];
 #pragma unroll
-    for (int k = 0; k < CT; ++k) acc[k] = 0.f;
-    float acc2[VL == 2 ? CT : 1];
+    for (int v = 0; v < VL; ++v)
 #pragma unroll
-    for (int k = 0; k < (VL == 2 ? CT : 1); ++k) acc2[k] = 0.f;
+      for (int k = 0; k < CT; ++k) accv[v][k] = 0.f;
     {
       float x0[VL][CT];
       load_x(c0, x0);
-      fma_batch(c0, w0, x0, acc, acc2);
+      fma_batch(c0, w0, x0, accv);
     }
     // rows longer than W: U batches of colIdx/val, then their dense rows, are
     // in flight before the (in-order) FMAs of the first one
-    constexpr int U = CT <= 1 ? 4 : (CT <= 4 ? 2 : 1);
+    // (wider virtual-lane groups already hold VL loads per lane)
+    constexpr int U0 = CT <= 1 ? 4 : (CT <= 4 ? 2 : 1);
+    constexpr int U = VL <= 2 ? U0 : (U0 * 2 / VL > 0 ? U0 * 2 / VL : 1);
     for (int base = s + W; base < f; base += U * W) {
       int c[U][VL];
       float w[U][VL];
@@ -167,13 +158,19 @@ par_rs_kernel(const ParArgs a) {
 #pragma unroll
       for (int u = 0; u < U; ++u) load_x(c[u], xv[u]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) fma_batch(c[u], w[u], xv[u], acc, acc2);
+      for (int u = 0; u < U; ++u) fma_batch(c[u], w[u], xv[u], accv);
     }
-    if constexpr (VL == 2) {
-      // tree level 1 of the 64-lane model: acc[l] = acc[2l+1] + acc[2l]
+    // the tree levels inside one physical lane (virtual lanes gl*VL .. +VL-1):
+    // acc[l] = acc[2l+1] + acc[2l] (kernels.hpp:193-199)
 #pragma unroll
-      for (int k = 0; k < CT; ++k) acc[k] = __fadd_rn(acc2[k], acc[k]);
-    }
+    for (int wv = VL; wv > 1; wv >>= 1)
+#pragma unroll
+      for (int v = 0; v < wv / 2; ++v)
+#pragma unroll
+        for (int k = 0; k < CT; ++k) accv[v][k] = __fadd_rn(accv[2 * v + 1][k], accv[2 * v][k]);
+    float acc[CT];
+#pragma unroll
+    for (int k = 0; k < CT; ++k) acc[k] = accv[0][k];
     // butterfly reduce-scatter levels (offsets 1..2^(HL-1))
     int cbase = 0;  // first column of the contiguous run this lane holds
 #pragma unroll

@@ -603,7 +603,44 @@ void launch_par_rs_w(ParArgs a, bool aligned, cudaStream_t s) {
   }
 }
 
-void launch_par_rs(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
+// Narrow dense rows (N <= 4): VL virtual lanes per physical lane, so a row
+// group is W/VL threads and several short rows share a warp; the tree levels
+// inside a physical lane run in registers (same order, kernels.hpp:193-199).
+template <int W, int VL>
+void launch_par_rs_narrow(ParArgs a, bool aligned, cudaStream_t s) {
+  const int N = a.N;
+  const int ct = N <= 1 ? 1 : N <= 2 ? 2 : 4;
+  a.ncol_tile = ct;
+  const bool v4 = aligned && (N % 4 == 0) && ct == 4;
+  switch (ct) {
+    case 1: launch_par_rs_t<W, VL, 1, false>(a, 1, s); break;
+    case 2: launch_par_rs_t<W, VL, 2, false>(a, 1, s); break;
+    default: v4 ? launch_par_rs_t<W, VL, 4, true>(a, 1, s) : launch_par_rs_t<W, VL, 4, false>(a, 1, s); break;
+  }
+}
+
+// Virtual lanes per physical lane for par-rs at lane_width 32, N <= 4 (the
+// results do not depend on it).  Measured on B200 (R-MAT s20 uniform, s22
+// heavy, the cfg5 8-way tail slice): 4 wins or ties everywhere except s22
+// heavy at N=2 (+6 %), 8 is best on narrow-row uniform graphs at N=1
+// (s20 uniform: 159 us at 1, 128 at 4, 112 at 8).
+int par_rs_vl(const spmk_csr_s* h, int W, int N) {
+  const long long env = env_ll("SPMK_PARRS_VL", 0);
+  if (env > 0) return (int)env;
+  if (W != 32 || N > 4) return 1;
+  const double M = (double)h->m, avg = (double)h->nnz / M;
+  const double var = std::max(0.0, (double)h->sum_len2 / M - avg * avg);
+  const double cv = avg > 0.0 ? std::sqrt(var) / avg : 0.0;
+  return (N == 1 && cv <= 1.0) ? 8 : 4;
+}
+
+void launch_par_rs(const ParArgs& a, int W, int vl, bool aligned, cudaStream_t s) {
+  if (a.N <= 4 && vl > 1) {
+    if (W == 32 && vl == 4) return launch_par_rs_narrow<32, 4>(a, aligned, s);
+    if (W == 32 && vl == 8) return launch_par_rs_narrow<32, 8>(a, aligned, s);
+    if (W == 64 && vl == 8) return launch_par_rs_narrow<64, 8>(a, aligned, s);
+    if (W == 16 && vl == 4) return launch_par_rs_narrow<16, 4>(a, aligned, s);
+  }
   switch (W) {
     case 2: launch_par_rs_w<2, 1>(a, aligned, s); break;
     case 4: launch_par_rs_w<4, 1>(a, aligned, s); break;
@@ -772,7 +809,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     if (id == SPMK_PAR_ROWSPLIT) {
       a.hub = hubs ? L : INT32_MAX;
       timing_record(1, s);
-      launch_par_rs(a, W, aligned, s);
+      launch_par_rs(a, W, par_rs_vl(h, W, N), aligned, s);
       timing_record(2, s);
     } else {
       const long long CH = W;

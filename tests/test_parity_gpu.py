@@ -280,3 +280,14 @@ def test_cfg2_full_size(orc):
         y = d.spmm(kid, x1)
         torch.cuda.synchronize()
         assert_bits(y.cpu().numpy(), orc.spmm(a, kid.index, x1h), f"cfg2 N=1 {kid.name}")
+
+
+@pytest.mark.parametrize("vl", [1, 4, 8])
+def test_par_rs_virtual_lanes(orc, dev_corpus, vl, monkeypatch):
+    """par-rs at lane_width 32 with VL virtual lanes per physical lane (the
+    tree levels inside a lane in registers): the same bits for every VL."""
+    monkeypatch.setenv("SPMK_PARRS_VL", str(vl))
+    for a, d in dev_corpus:
+        for n in (1, 2, 3, 4):
+            x = orc.make_dense(a.k, n, 97 * n + vl)
+            assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), f"{a.name} n={n} vl={vl}")
