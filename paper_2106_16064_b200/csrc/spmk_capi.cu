@@ -620,9 +620,10 @@ void launch_par_rs_narrow(ParArgs a, bool aligned, cudaStream_t s) {
 }
 
 // Virtual lanes per physical lane for par-rs at lane_width 32, N <= 4 (the
-// results do not depend on it).  Measured on B200 (R-MAT s20 uniform, s22
-// heavy, the cfg5 8-way tail slice): 4 wins or ties everywhere except s22
-// heavy at N=2 (+6 %), 8 is best on narrow-row uniform graphs at N=1
+// results do not depend on it).  Measured on B200: rows averaging >= 24
+// nonzeros fill a 32-lane group (cfg5 8-way slices 0-3, avg 27..443: VL=1
+// 0.36-0.41 ms vs VL=4 0.41-0.45 ms); shorter rows want narrow groups (tail
+// slice, avg 4.5: 0.75 -> 0.60 ms at VL=4), 8 on low-cv graphs at N=1
 // (s20 uniform: 159 us at 1, 128 at 4, 112 at 8).
 int par_rs_vl(const spmk_csr_s* h, int W, int N) {
   const long long env = env_ll("SPMK_PARRS_VL", 0);
@@ -631,6 +632,7 @@ int par_rs_vl(const spmk_csr_s* h, int W, int N) {
   const double M = (double)h->m, avg = (double)h->nnz / M;
   const double var = std::max(0.0, (double)h->sum_len2 / M - avg * avg);
   const double cv = avg > 0.0 ? std::sqrt(var) / avg : 0.0;
+  if (avg >= 24.0) return 1;
   return (N == 1 && cv <= 1.0) ? 8 : 4;
 }
 
