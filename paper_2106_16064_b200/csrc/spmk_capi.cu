@@ -698,6 +698,25 @@ void launch_par_ws(const ParArgs& a, int W, bool aligned, cudaStream_t s) {
   else launch_par_ws_tt<4, 5>(a, W, aligned, s);
 }
 
+// seq-rs tile (nonzeros whose rows start in one span): 256; at N <= 2 (one
+// lane per unit) shrunk on small matrices so there are >= 256 tiles per SM
+// (measured: R-MAT s16 N=1 87 -> 23.5 us, s18 heavy N=1 281 -> 133 us; at
+// N >= 4 smaller tiles lost 5-40 %, sweep r01n vs r01o).  Tiles hold whole
+// rows, so the size never changes the results.
+long long rs_tile_nnz(long long nnz, int N) {
+  if (N > 2) return 256;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  long long ts = 256;
+  while (ts > 32 && nnz / ts < (long long)sms * 256) ts >>= 1;
+  return ts;
+}
+
 // Tile sizes (nonzeros per work unit).  Any multiple of the chunk keeps the
 // results bit-exact; these are pure performance knobs (env overridable).
 long long tile_chunks(long long chunk, long long target) {
@@ -766,7 +785,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.N = N;
     a.cvvec = ((uintptr_t)h->col % 16 == 0) && ((uintptr_t)h->val % 16 == 0);
     if (id == SPMK_SEQ_ROWSPLIT) {
-      const long long TS = std::max(1LL, env_ll("SPMK_SEQ_TILE_NNZ", 256));
+      const long long TS = std::max(1LL, env_ll("SPMK_SEQ_TILE_NNZ", rs_tile_nnz(h->nnz, N)));
       Plan& p = get_rs_desc(h, TS, L, hubs ? hub : nullptr, s);
       a.nunits = (int)p.ntiles;
       a.desc = p.desc;
