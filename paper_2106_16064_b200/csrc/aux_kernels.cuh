@@ -246,22 +246,34 @@ __global__ void zero_all_kernel(float* __restrict__ Y, long long total) {
 // contract; the adds are the only serial part).
 constexpr int kFixupWarps = 8;
 constexpr int kFixupBuf = 1024;  // floats per warp per batch
-__global__ void __launch_bounds__(kFixupWarps * 32)
-fixup_kernel(const int* __restrict__ list, int nlong,
-             const int* __restrict__ crp, const int* __restrict__ rid,
-             const float* __restrict__ H, const float* __restrict__ Tsl,
-             float* __restrict__ Y, int N, long long TS, long long CH) {
-  __shared__ float sm[kFixupWarps][kFixupBuf];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float* buf = sm[w];
-  const long long T = TS / CH;
-  for (long long li = (long long)blockIdx.x * kFixupWarps + w; li < nlong;
-       li += (long long)gridDim.x * kFixupWarps) {
+
+// Per long row, precomputed with the plan: {output row, owner tile t1, first
+// and last partial slot q0..q1} — the fixup then starts with one 16-byte load
+// instead of the list -> rowPtr -> rid chain (most long rows have 1-2
+// partials, so that chain was most of the fixup's time).
+__global__ void long_info_kernel(const int* __restrict__ list, int nlong, const int* __restrict__ crp,
+                                 const int* __restrict__ rid, long long TS, long long CH,
+                                 int4* __restrict__ info) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < nlong;
+       li += (long long)gridDim.x * blockDim.x) {
     const int c = list[li];
     const long long s = crp[c], f = crp[c + 1];
     const long long t1 = s / TS;
-    const long long q0 = (t1 + 1) * T, q1 = (f - 1) / CH;
-    const long long yrow = (long long)rid[c] * N;
+    info[li] = make_int4(rid[c], (int)t1, (int)((t1 + 1) * (TS / CH)), (int)((f - 1) / CH));
+  }
+}
+
+__global__ void __launch_bounds__(kFixupWarps * 32)
+fixup_kernel(const int4* __restrict__ info, int nlong, const float* __restrict__ H,
+             const float* __restrict__ Tsl, float* __restrict__ Y, int N) {
+  __shared__ float sm[kFixupWarps][kFixupBuf];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = sm[w];
+  for (long long li = (long long)blockIdx.x * kFixupWarps + w; li < nlong;
+       li += (long long)gridDim.x * kFixupWarps) {
+    const int4 d = info[li];
+    const long long t1 = d.y, q0 = d.z, q1 = d.w;
+    const long long yrow = (long long)d.x * N;
     for (int j0 = 0; j0 < N; j0 += 32) {
       const int ncol = min(32, N - j0);
       float acc = (lane < ncol) ? Tsl[t1 * N + j0 + lane] : 0.f;

@@ -69,6 +69,7 @@ struct Plan {
   long long ntiles = 0;
   long long TS = 0, CH = 0, EXT = 0;
   int* longrows = nullptr;
+  int4* longinfo = nullptr;  // ws plans: fixup descriptors (long_info_kernel)
   int nlong = 0;
   std::vector<int> hrows;  // hub plans: hub rows in ascending order (host copy)
   std::vector<int> hlen;   // hub plans: hub row lengths in launch order
@@ -174,6 +175,7 @@ void free_handle(spmk_csr_s* h) {
     cudaFree(kv.second.rlo);
     cudaFree(kv.second.desc);
     cudaFree(kv.second.longrows);
+    cudaFree(kv.second.longinfo);
   }
   cudaFree(h->scratch);
   for (auto& kv : h->hub_layouts) {
@@ -260,6 +262,11 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EX
   CK(cudaMemcpyAsync(&p.nlong, cnt, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   cudaFree(cnt);
+  if (p.nlong > 0) {
+    p.longinfo = dev_alloc<int4>((size_t)p.nlong);
+    long_info_kernel<<<grid_for(p.nlong), 256, 0, s>>>(p.longrows, p.nlong, h->crp, h->rid, TS, CH, p.longinfo); LAUNCHED(1);
+    CK(cudaGetLastError());
+  }
   return h->plans.emplace(key, p).first->second;
 }
 
@@ -812,8 +819,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_seq<true>(a, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<std::min((p.nlong + kFixupWarps - 1) / kFixupWarps, 148 * 8), kFixupWarps * 32, 0, s>>>(
-            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
+        fixup_kernel<<<(p.nlong + kFixupWarps - 1) / kFixupWarps, kFixupWarps * 32, 0, s>>>(
+            p.longinfo, p.nlong, a.H, a.Tsl, d_y, N); LAUNCHED(1);
     }
   } else {
     ParArgs a{};
@@ -850,8 +857,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws(a, W, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<std::min((p.nlong + kFixupWarps - 1) / kFixupWarps, 148 * 8), kFixupWarps * 32, 0, s>>>(
-            p.longrows, p.nlong, h->crp, h->rid, a.H, a.Tsl, d_y, N, TS, CH); LAUNCHED(1);
+        fixup_kernel<<<(p.nlong + kFixupWarps - 1) / kFixupWarps, kFixupWarps * 32, 0, s>>>(
+            p.longinfo, p.nlong, a.H, a.Tsl, d_y, N); LAUNCHED(1);
     }
   }
   if (fork) CK(cudaStreamWaitEvent(s, h->ev_join, 0));
