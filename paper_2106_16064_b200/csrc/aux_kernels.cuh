@@ -263,60 +263,106 @@ __global__ void long_info_kernel(const int* __restrict__ list, int nlong, const 
   }
 }
 
+// One long row folded by the whole warp (all lanes converged).
+__device__ __forceinline__ void fixup_row(const int4 d, int lane, float* buf, const float* __restrict__ H,
+                                          const float* __restrict__ Tsl, float* __restrict__ Y, int N) {
+  const long long t1 = d.y, q0 = d.z, q1 = d.w;
+  const long long yrow = (long long)d.x * N;
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int ncol = min(32, N - j0);
+    float acc = (lane < ncol) ? Tsl[t1 * N + j0 + lane] : 0.f;
+    if (ncol == 32) {
+      // 32 columns: lane j reads column j of every partial directly (one
+      // 128-B line per partial), 16 partials in flight ahead of the adds
+      // (measured: N=64 whole call 461 -> 417 us, N=32 291 -> 287 us;
+      // prefetching the next 16 before the adds was slower)
+      const float* src = H + j0 + lane;
+      long long q = q0;
+      for (; q + 16 <= q1 + 1; q += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = src[(q + u) * N];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, v[u]);
+      }
+      for (; q <= q1; ++q) acc = __fadd_rn(acc, src[q * N]);
+      Y[yrow + j0 + lane] = acc;
+      continue;
+    }
+    const long long qpb = kFixupBuf / ncol;  // partials per batch
+    for (long long qb = q0; qb <= q1; qb += qpb) {
+      const int nqb = (int)min(qpb, q1 + 1 - qb);
+      const int cnt = nqb * ncol;
+      __syncwarp();
+      if (ncol == N) {  // whole rows of H: one contiguous range
+        const float* src = H + qb * N;
+#pragma unroll 8
+        for (int i = lane; i < cnt; i += 32) buf[i] = src[i];
+      } else {
+#pragma unroll 4
+        for (int i = lane; i < cnt; i += 32) buf[i] = H[(qb + i / ncol) * N + j0 + i % ncol];
+      }
+      __syncwarp();
+      if (lane < ncol) {
+#pragma unroll 8
+        for (int qq = 0; qq < nqb; ++qq) acc = __fadd_rn(acc, buf[qq * ncol + lane]);
+      }
+    }
+    if (lane < ncol) Y[yrow + j0 + lane] = acc;
+  }
+}
+
+// Rows with more than kFixupLaneMax partials are "big": the plan puts them
+// first in the descriptor list (nbig of them) so they spread over warps.
+constexpr int kFixupLaneMax = 32;
+inline int fixup_blocks(int nlong, int nbig, int N) {
+  if (N != 1) return (nlong + kFixupWarps - 1) / kFixupWarps;
+  const int b_big = (nbig + kFixupWarps - 1) / kFixupWarps;
+  const int b_small = (nlong - nbig + kFixupWarps * 32 - 1) / (kFixupWarps * 32);
+  return b_big > b_small ? b_big : (b_small > 0 ? b_small : 1);
+}
+
 __global__ void __launch_bounds__(kFixupWarps * 32)
-fixup_kernel(const int4* __restrict__ info, int nlong, const float* __restrict__ H,
+fixup_kernel(const int4* __restrict__ info, int nlong, int nbig, const float* __restrict__ H,
              const float* __restrict__ Tsl, float* __restrict__ Y, int N) {
   __shared__ float sm[kFixupWarps][kFixupBuf];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float* buf = sm[w];
-  for (long long li = (long long)blockIdx.x * kFixupWarps + w; li < nlong;
-       li += (long long)gridDim.x * kFixupWarps) {
-    const int4 d = info[li];
-    const long long t1 = d.y, q0 = d.z, q1 = d.w;
-    const long long yrow = (long long)d.x * N;
-    for (int j0 = 0; j0 < N; j0 += 32) {
-      const int ncol = min(32, N - j0);
-      float acc = (lane < ncol) ? Tsl[t1 * N + j0 + lane] : 0.f;
-      if (ncol == 32) {
-        // 32 columns: lane j reads column j of every partial directly (one
-        // 128-B line per partial), 16 partials in flight ahead of the adds
-        // (measured: N=64 whole call 461 -> 417 us, N=32 291 -> 287 us;
-        // prefetching the next 16 before the adds was slower)
-        const float* src = H + j0 + lane;
-        long long q = q0;
-        for (; q + 16 <= q1 + 1; q += 16) {
-          float v[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = src[(q + u) * N];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) acc = __fadd_rn(acc, v[u]);
+  if (N == 1) {
+    // One column: the big rows one per warp (the chain of adds is the serial
+    // part), then every other row folded by one lane, 32 rows per warp (most
+    // long rows have 1-2 partials).
+    const long long gw = (long long)blockIdx.x * kFixupWarps + w, nw = (long long)gridDim.x * kFixupWarps;
+    for (long long li = gw; li < nbig; li += nw) fixup_row(info[li], lane, buf, H, Tsl, Y, N);
+    for (long long l0 = nbig + gw * 32; l0 < nlong; l0 += nw * 32) {
+      const long long li = l0 + lane;
+      const bool mine = li < nlong;
+      const int4 d = mine ? info[li] : make_int4(0, 0, 0, -1);
+      const bool small = mine && d.w - d.z < kFixupLaneMax;
+      if (small) {
+        float acc = Tsl[d.y];
+        int q = d.z;
+        for (; q + 4 <= d.w + 1; q += 4) {
+          const float v0 = H[q], v1 = H[q + 1], v2 = H[q + 2], v3 = H[q + 3];
+          acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
         }
-        for (; q <= q1; ++q) acc = __fadd_rn(acc, src[q * N]);
-        Y[yrow + j0 + lane] = acc;
-        continue;
+        for (; q <= d.w; ++q) acc = __fadd_rn(acc, H[q]);
+        Y[d.x] = acc;
       }
-      const long long qpb = kFixupBuf / ncol;  // partials per batch
-      for (long long qb = q0; qb <= q1; qb += qpb) {
-        const int nqb = (int)min(qpb, q1 + 1 - qb);
-        const int cnt = nqb * ncol;
-        __syncwarp();
-        if (ncol == N) {  // whole rows of H: one contiguous range
-          const float* src = H + qb * N;
-#pragma unroll 8
-          for (int i = lane; i < cnt; i += 32) buf[i] = src[i];
-        } else {
-#pragma unroll 4
-          for (int i = lane; i < cnt; i += 32) buf[i] = H[(qb + i / ncol) * N + j0 + i % ncol];
-        }
-        __syncwarp();
-        if (lane < ncol) {
-#pragma unroll 8
-          for (int qq = 0; qq < nqb; ++qq) acc = __fadd_rn(acc, buf[qq * ncol + lane]);
-        }
+      unsigned big = __ballot_sync(0xffffffffu, mine && !small);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const int4 db = make_int4(__shfl_sync(0xffffffffu, d.x, src), __shfl_sync(0xffffffffu, d.y, src),
+                                  __shfl_sync(0xffffffffu, d.z, src), __shfl_sync(0xffffffffu, d.w, src));
+        fixup_row(db, lane, buf, H, Tsl, Y, N);
       }
-      if (lane < ncol) Y[yrow + j0 + lane] = acc;
     }
+    return;
   }
+  for (long long li = (long long)blockIdx.x * kFixupWarps + w; li < nlong;
+       li += (long long)gridDim.x * kFixupWarps)
+    fixup_row(info[li], lane, buf, H, Tsl, Y, N);
 }
 
 // |val| (for the north-star bound sum_j |a_ij x_j| computed on the device).

@@ -69,8 +69,9 @@ struct Plan {
   long long ntiles = 0;
   long long TS = 0, CH = 0, EXT = 0;
   int* longrows = nullptr;
-  int4* longinfo = nullptr;  // ws plans: fixup descriptors (long_info_kernel)
+  int4* longinfo = nullptr;  // ws plans: fixup descriptors (long_info_kernel), big rows first
   int nlong = 0;
+  int nbig = 0;              // ws plans: long rows with > kFixupLaneMax partials
   std::vector<int> hrows;  // hub plans: hub rows in ascending order (host copy)
   std::vector<int> hlen;   // hub plans: hub row lengths in launch order
 };
@@ -266,6 +267,15 @@ Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EX
     p.longinfo = dev_alloc<int4>((size_t)p.nlong);
     long_info_kernel<<<grid_for(p.nlong), 256, 0, s>>>(p.longrows, p.nlong, h->crp, h->rid, TS, CH, p.longinfo); LAUNCHED(1);
     CK(cudaGetLastError());
+    // big rows first (stable partition on the host, once per plan)
+    std::vector<int4> info((size_t)p.nlong);
+    CK(cudaMemcpyAsync(info.data(), p.longinfo, sizeof(int4) * info.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    auto it = std::stable_partition(info.begin(), info.end(),
+                                    [](const int4& d) { return d.w - d.z >= kFixupLaneMax; });
+    p.nbig = (int)(it - info.begin());
+    CK(cudaMemcpyAsync(p.longinfo, info.data(), sizeof(int4) * info.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
   }
   return h->plans.emplace(key, p).first->second;
 }
@@ -819,8 +829,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_seq<true>(a, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<(p.nlong + kFixupWarps - 1) / kFixupWarps, kFixupWarps * 32, 0, s>>>(
-            p.longinfo, p.nlong, a.H, a.Tsl, d_y, N); LAUNCHED(1);
+        fixup_kernel<<<fixup_blocks(p.nlong, p.nbig, N), kFixupWarps * 32, 0, s>>>(
+            p.longinfo, p.nlong, p.nbig, a.H, a.Tsl, d_y, N); LAUNCHED(1);
     }
   } else {
     ParArgs a{};
@@ -857,8 +867,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws(a, W, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0)
-        fixup_kernel<<<(p.nlong + kFixupWarps - 1) / kFixupWarps, kFixupWarps * 32, 0, s>>>(
-            p.longinfo, p.nlong, a.H, a.Tsl, d_y, N); LAUNCHED(1);
+        fixup_kernel<<<fixup_blocks(p.nlong, p.nbig, N), kFixupWarps * 32, 0, s>>>(
+            p.longinfo, p.nlong, p.nbig, a.H, a.Tsl, d_y, N); LAUNCHED(1);
     }
   }
   if (fork) CK(cudaStreamWaitEvent(s, h->ev_join, 0));
