@@ -316,9 +316,10 @@ __device__ __forceinline__ void fixup_row(const int4 d, int lane, float* buf, co
 // first in the descriptor list (nbig of them) so they spread over warps.
 constexpr int kFixupLaneMax = 32;
 inline int fixup_blocks(int nlong, int nbig, int N) {
-  if (N != 1) return (nlong + kFixupWarps - 1) / kFixupWarps;
+  if (N > 16) return (nlong + kFixupWarps - 1) / kFixupWarps;
+  const int rpw = 32 / N;
   const int b_big = (nbig + kFixupWarps - 1) / kFixupWarps;
-  const int b_small = (nlong - nbig + kFixupWarps * 32 - 1) / (kFixupWarps * 32);
+  const int b_small = (nlong - nbig + kFixupWarps * rpw - 1) / (kFixupWarps * rpw);
   return b_big > b_small ? b_big : (b_small > 0 ? b_small : 1);
 }
 
@@ -350,6 +351,41 @@ fixup_kernel(const int4* __restrict__ info, int nlong, int nbig, const float* __
         Y[d.x] = acc;
       }
       unsigned big = __ballot_sync(0xffffffffu, mine && !small);
+      while (big) {
+        const int src = __ffs(big) - 1;
+        big &= big - 1;
+        const int4 db = make_int4(__shfl_sync(0xffffffffu, d.x, src), __shfl_sync(0xffffffffu, d.y, src),
+                                  __shfl_sync(0xffffffffu, d.z, src), __shfl_sync(0xffffffffu, d.w, src));
+        fixup_row(db, lane, buf, H, Tsl, Y, N);
+      }
+    }
+    return;
+  }
+  if (N <= 16) {
+    // Narrow Y (2 <= N <= 16): the same with N lanes per small row (lane = row
+    // slot x column), 32/N rows per warp — most long rows have 1-2 partials.
+    const int rpw = 32 / N;                 // rows per warp
+    const int rs = lane / N, c = lane - rs * N;
+    const long long gw = (long long)blockIdx.x * kFixupWarps + w, nw = (long long)gridDim.x * kFixupWarps;
+    for (long long li = gw; li < nbig; li += nw) fixup_row(info[li], lane, buf, H, Tsl, Y, N);
+    for (long long l0 = nbig + gw * rpw; l0 < nlong; l0 += nw * rpw) {
+      const long long li = l0 + rs;
+      const bool mine = rs < rpw && li < nlong;
+      const int4 d = mine ? info[li] : make_int4(0, 0, 0, -1);
+      const bool small = mine && d.w - d.z < kFixupLaneMax;
+      if (small) {
+        const float* hc = H + c;
+        float acc = Tsl[(long long)d.y * N + c];
+        long long q = d.z;
+        for (; q + 4 <= d.w + 1; q += 4) {
+          const float v0 = hc[q * N], v1 = hc[(q + 1) * N], v2 = hc[(q + 2) * N], v3 = hc[(q + 3) * N];
+          acc = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc, v0), v1), v2), v3);
+        }
+        for (; q <= d.w; ++q) acc = __fadd_rn(acc, hc[q * N]);
+        Y[(long long)d.x * N + c] = acc;
+      }
+      // (rows past nbig are small by construction; kept for safety)
+      unsigned big = __ballot_sync(0xffffffffu, mine && !small && c == 0);
       while (big) {
         const int src = __ffs(big) - 1;
         big &= big - 1;
