@@ -47,7 +47,26 @@ pagerank_update_kernel(const float* __restrict__ y, float* __restrict__ r, const
   const long long m4 = vec ? (m & ~3LL) : 0;
   const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
-  for (long long i = 4 * tid; i < m4; i += 4 * nth) {
+  // two 16-byte groups per thread per step, all six loads issued first
+  // (HBM-bound: more bytes in flight per thread)
+  long long i = 4 * tid;
+  for (; i + 4 * nth < m4; i += 8 * nth) {
+    const long long i2 = i + 4 * nth;
+    const float4 yv = *reinterpret_cast<const float4*>(y + i), yv2 = *reinterpret_cast<const float4*>(y + i2);
+    float4 rv = *reinterpret_cast<const float4*>(r + i), rv2 = *reinterpret_cast<const float4*>(r + i2);
+    const int4 cv = *reinterpret_cast<const int4*>(counts + i), cv2 = *reinterpret_cast<const int4*>(counts + i2);
+    pr_elem(yv.x, rv.x, cv.x, alpha, base, l1, dang);
+    pr_elem(yv.y, rv.y, cv.y, alpha, base, l1, dang);
+    pr_elem(yv.z, rv.z, cv.z, alpha, base, l1, dang);
+    pr_elem(yv.w, rv.w, cv.w, alpha, base, l1, dang);
+    pr_elem(yv2.x, rv2.x, cv2.x, alpha, base, l1, dang);
+    pr_elem(yv2.y, rv2.y, cv2.y, alpha, base, l1, dang);
+    pr_elem(yv2.z, rv2.z, cv2.z, alpha, base, l1, dang);
+    pr_elem(yv2.w, rv2.w, cv2.w, alpha, base, l1, dang);
+    *reinterpret_cast<float4*>(r + i) = rv;
+    *reinterpret_cast<float4*>(r + i2) = rv2;
+  }
+  for (; i < m4; i += 4 * nth) {
     const float4 yv = *reinterpret_cast<const float4*>(y + i);
     float4 rv = *reinterpret_cast<const float4*>(r + i);
     const int4 cv = *reinterpret_cast<const int4*>(counts + i);
