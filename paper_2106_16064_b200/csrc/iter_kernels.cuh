@@ -121,9 +121,29 @@ pagerank_update_p2p_kernel(const float* __restrict__ y, const float* __restrict_
   __shared__ double s1[kIterThreads / 32], s2[kIterThreads / 32];
   const float base = (float)st[0];
   double l1 = 0.0, dang = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x) {
-    float rv = xcur[row0 + i];  // old value in, new value out (residual inside)
+  // four rows per thread per step with every load issued first (the same
+  // per-thread element order as one row per step: the residual bits match)
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * nth < m; i += 4 * nth) {
+    float yv[4], rv[4];
+    int cv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      yv[u] = y[i + u * nth];
+      rv[u] = xcur[row0 + i + u * nth];  // old value in, new value out (residual inside)
+      cv[u] = counts[row0 + i + u * nth];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pr_elem(yv[u], rv[u], cv[u], alpha, base, l1, dang);
+#pragma unroll
+      for (int q = 0; q < kMaxPeers; ++q)
+        if (q < npeers) peers.p[q][row0 + i + u * nth] = rv[u];
+    }
+  }
+  for (; i < m; i += nth) {
+    float rv = xcur[row0 + i];
     pr_elem(y[i], rv, counts[row0 + i], alpha, base, l1, dang);
 #pragma unroll
     for (int q = 0; q < kMaxPeers; ++q)
