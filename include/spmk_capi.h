@@ -99,7 +99,7 @@ spmk_status spmk_csr_create(int64_t num_rows, int64_t num_cols, int64_t nnz,
 /* Same, from int32 DEVICE arrays already in HBM (e.g. the device generator);
  * the call synchronizes the device first, so producers on any stream are done.
  * copy=0 borrows the arrays (caller keeps them alive), copy=1 duplicates.
- * Validation is done on the device (canonical rows, bounds). */
+ * Validation is done on the device (row_ptr shape, column bounds). */
 spmk_status spmk_csr_create_device(int64_t num_rows, int64_t num_cols,
                                    int64_t nnz, const int32_t* d_row_ptr,
                                    const int32_t* d_col_idx,
@@ -120,6 +120,20 @@ spmk_status spmk_csr_info(spmk_csr_t a, int64_t* num_rows, int64_t* num_cols,
 spmk_status spmk_csr_device_arrays(spmk_csr_t a, const int32_t** d_row_ptr,
                                    const int32_t** d_col_idx,
                                    const float** d_values);
+/* validate (csr.hpp:95-119) of the resident CSR.  Handle creation checks what
+ * the device path needs for safety (row_ptr shape, column range: SPMK_EINVAL
+ * otherwise) but, like the reference's spmm_* (kernels.hpp:157-455, which
+ * never call validate), accepts rows whose columns are not strictly
+ * increasing and computes in position order; this call reports that case as
+ * SPMK_EINVAL with the reference's message. */
+spmk_status spmk_csr_validate(spmk_csr_t a);
+/* Per-handle performance knobs (no effect on any result bit):
+ * "seq_tile_nnz", "seq_ext", "parws_ext", "parws_t", "parrs_vl", "hub_nnz",
+ * "hub_two_pass", "hub_smem", "l2_persist".  Initialised at creation from the
+ * environment (SPMK_<KEY upper-case>), read by every later spmm on the handle;
+ * a changed knob takes effect on the next call (plans are cached per shape). */
+spmk_status spmk_csr_set_tuning(spmk_csr_t a, const char* key, int64_t value);
+spmk_status spmk_csr_get_tuning(spmk_csr_t a, const char* key, int64_t* value);
 /* Download back to the reference layout (int64 indices). */
 spmk_status spmk_csr_download(spmk_csr_t a, int64_t* row_ptr, int64_t* col_idx,
                               float* values);

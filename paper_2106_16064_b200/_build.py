@@ -20,13 +20,22 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+OBJ_DIR = os.path.join(PKG, "build")
+
+
+def _units():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
+
+
+def _headers():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cuh", ".h"))] + [
+        os.path.join(ROOT, "include", "spmk_capi.h")]
 
 
 def _sources():
-    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))] + [
-        os.path.join(ROOT, "include", "spmk_capi.h")]
+    return _units() + _headers()
 
 
 def _stale(target, deps):
@@ -37,11 +46,30 @@ def _stale(target, deps):
 
 
 def build_library(force: bool = False, verbose: bool = True) -> str:
-    if force or _stale(LIB, _sources()):
-        cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "spmk_capi.cu")]
+    """Compile every translation unit of csrc/ (in parallel) and link
+    libspmk_b200.so.  NCCL is not linked: the multi-GPU layer resolves it at
+    run time (dlopen), so the library loads on hosts without NCCL."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    headers = _headers()
+    jobs = []
+    for cu in _units():
+        obj = os.path.join(OBJ_DIR, os.path.basename(cu)[:-3] + ".o")
+        if force or _stale(obj, [cu] + headers):
+            jobs.append([NVCC, *NVCC_FLAGS, "-c", "-o", obj, cu])
+    objs = [os.path.join(OBJ_DIR, os.path.basename(cu)[:-3] + ".o") for cu in _units()]
+
+    def run(cmd):
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+            list(ex.map(run, jobs))
+    if force or jobs or _stale(LIB, objs):
+        run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp", *objs, "-ldl"])
         os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -40,23 +40,39 @@ __global__ void widen_kernel(const int* __restrict__ in, long long* __restrict__
     out[i] = in[i];
 }
 
-// validate (csr.hpp:95-119) on the device.  err bits: 1 row_ptr, 2 column
-// range, 4 column order.
-__global__ void validate_kernel(const int* __restrict__ rp, const int* __restrict__ col,
-                                int m, int k, long long nnz, int* __restrict__ err) {
+// validate (csr.hpp:95-119) on the device, nonzero-parallel.  err bits:
+// 1 row_ptr, 2 column range, 4 column order.  Pass 1 (one thread per row)
+// checks row_ptr and marks every row start in a bitmap; pass 2 (one thread per
+// nonzero) checks the column range and, unless the position starts a row, the
+// strict order against its predecessor.  Work is O(M + nnz) with no serial
+// per-row loop, so hub rows cost nothing extra.
+__global__ void validate_rows_kernel(const int* __restrict__ rp, int m, long long nnz,
+                                     unsigned* __restrict__ starts, int* __restrict__ err) {
+  int bad = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const int s = rp[i], f = rp[i + 1];
-    if (s > f || s < 0 || f > nnz) { atomicOr(err, 1); continue; }
-    for (int e = s; e < f; ++e) {
-      const int c = col[e];
-      if (c < 0 || c >= k) atomicOr(err, 2);
-      if (e > s && c <= col[e - 1]) atomicOr(err, 4);
+    if (s > f || s < 0 || f > nnz) {
+      bad |= 1;
+    } else if (s < f) {
+      atomicOr(starts + (s >> 5), 1u << (s & 31));
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (rp[0] != 0 || (long long)rp[m] != nnz) atomicOr(err, 1);
+    if (rp[0] != 0 || (long long)rp[m] != nnz) bad |= 1;
   }
+  if (bad) atomicOr(err, bad);
+}
+__global__ void validate_cols_kernel(const int* __restrict__ col, long long nnz, int k,
+                                     const unsigned* __restrict__ starts, int* __restrict__ err) {
+  int bad = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int c = col[e];
+    if (c < 0 || c >= k) bad |= 2;
+    if (e > 0 && !((starts[e >> 5] >> (e & 31)) & 1u) && c <= col[e - 1]) bad |= 4;
+  }
+  if (bad) atomicOr(err, bad);
 }
 
 // row-length moments for extract_features (csr.hpp:166-181): exact integer
@@ -231,6 +247,16 @@ __global__ void zero_rows_kernel(const int* __restrict__ erow, int ne, int N,
   }
 }
 // All of Y zero (nnz == 0 or every row empty).
+// Rows with >= L nonzeros: {compact row, length}.
+__global__ void hub_rows_kernel(const int* __restrict__ crp, int mne, int L, int2* __restrict__ out,
+                                int* __restrict__ count) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < mne;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int len = crp[c + 1] - crp[c];
+    if (len >= L) out[atomicAdd(count, 1)] = make_int2((int)c, len);
+  }
+}
+
 __global__ void zero_all_kernel(float* __restrict__ Y, long long total) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x)

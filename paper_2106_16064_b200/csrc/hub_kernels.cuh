@@ -28,16 +28,6 @@ constexpr int kHubChunk = kHubProducers * 32;   // positions per shared-memory c
 template <int CW>
 constexpr int hub_smem_bytes() { return 2 * kHubChunk * CW * 4; }  // double buffer (57,344 B at CW = 32)
 
-// Rows with >= L nonzeros: {compact row, length}.
-__global__ void hub_rows_kernel(const int* __restrict__ crp, int mne, int L, int2* __restrict__ out,
-                                int* __restrict__ count) {
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < mne;
-       c += (long long)gridDim.x * blockDim.x) {
-    const int len = crp[c + 1] - crp[c];
-    if (len >= L) out[atomicAdd(count, 1)] = make_int2((int)c, len);
-  }
-}
-
 struct HubArgs {
   const int* __restrict__ hubs;  // compact rows, longest first
   const int* __restrict__ crp;

@@ -163,7 +163,8 @@ def exchange_slices(x, bounds: List[int], group=None) -> None:
     for g in range(len(bounds) - 1):
         lo, hi = int(bounds[g]), int(bounds[g + 1])
         if hi > lo:
-            dist.broadcast(x[lo:hi], src=g, group=group)
+            src = g if group is None else dist.get_global_rank(group, g)  # src is a global rank
+            dist.broadcast(x[lo:hi], src=src, group=group)
 
 
 def _ipc_handle(t) -> bytes:

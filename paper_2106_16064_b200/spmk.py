@@ -68,6 +68,9 @@ _SIGS = {
     "spmk_csr_slice": ([vp, i64, i64, C.c_int, P(vp)], C.c_int),
     "spmk_csr_abs_copy": ([vp, P(vp)], C.c_int),
     "spmk_csr_destroy": ([vp], C.c_int),
+    "spmk_csr_validate": ([vp], C.c_int),
+    "spmk_csr_set_tuning": ([vp, C.c_char_p, i64], C.c_int),
+    "spmk_csr_get_tuning": ([vp, C.c_char_p, P(i64)], C.c_int),
     "spmk_csr_info": ([vp, P(i64), P(i64), P(i64), P(i64), P(i64)], C.c_int),
     "spmk_csr_device_arrays": ([vp, P(vp), P(vp), P(vp)], C.c_int),
     "spmk_csr_download": ([vp, P(i64), P(i64), P(f32)], C.c_int),
@@ -334,6 +337,20 @@ class DeviceCsr:
             pass
 
     # queries
+    def validate(self) -> None:
+        """validate (csr.hpp:95-119): raises Error unless every row's columns
+        are strictly increasing (bounds are checked at creation)."""
+        _check(self.lib.spmk_csr_validate(self._h))
+
+    def set_tuning(self, key: str, value: int) -> None:
+        """Per-handle performance knob (never changes a result bit)."""
+        _check(self.lib.spmk_csr_set_tuning(self._h, key.encode(), int(value)))
+
+    def get_tuning(self, key: str) -> int:
+        v = i64()
+        _check(self.lib.spmk_csr_get_tuning(self._h, key.encode(), C.byref(v)))
+        return v.value
+
     def download(self) -> CsrMatrix:
         rp = np.empty(self.num_rows + 1, np.int64)
         ci = np.empty(max(self.nnz, 1), np.int64)
@@ -382,6 +399,11 @@ class DeviceCsr:
         return m.value, s.value
 
     # compute
+    def _check_out(self, y, n):
+        if not (isinstance(y, np.ndarray) and y.dtype == np.float32 and y.flags.c_contiguous
+                and y.shape == (self.num_rows, n)):
+            raise Error(f"Y must be a C-contiguous float32 array of shape ({self.num_rows}, {n})")
+
     def spmm_ptr(self, kid: KernelId, d_x: int, n: int, d_y: int, stream: int = 0,
                  cfg: Optional[KernelConfig] = None) -> None:
         """Y = A*X on device pointers (asynchronous on `stream`)."""
@@ -393,12 +415,18 @@ class DeviceCsr:
         """torch CUDA tensors in/out (fp32, row-major)."""
         import torch
 
-        assert x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+        if not (x.is_cuda and x.dtype == torch.float32 and x.is_contiguous() and x.dim() in (1, 2)):
+            raise Error("X must be a contiguous float32 CUDA tensor of 1 or 2 dimensions")
         n = x.shape[1] if x.dim() == 2 else 1
         if x.shape[0] != self.num_cols:
             raise Error(f"dimension mismatch: A is {self.num_rows}x{self.num_cols}, X has {x.shape[0]} rows")
         if y is None:
             y = torch.empty((self.num_rows, n), dtype=torch.float32, device=x.device)
+        elif not (y.is_cuda and y.dtype == torch.float32 and y.is_contiguous() and y.device == x.device
+                  and y.numel() == self.num_rows * n and (y.dim() == 2 and tuple(y.shape) == (self.num_rows, n)
+                                                          or y.dim() == 1 and n == 1)):
+            raise Error(f"Y must be a contiguous float32 CUDA tensor of shape ({self.num_rows}, {n}) "
+                        f"on {x.device}")
         st = stream if stream is not None else torch.cuda.current_stream(x.device)
         self.spmm_ptr(kid, x.data_ptr(), n, y.data_ptr(), st.cuda_stream, cfg)
         return y
@@ -410,8 +438,11 @@ class DeviceCsr:
     def spmm_host(self, kid: KernelId, x: np.ndarray, cfg: Optional[KernelConfig] = None,
                   stream: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float32)
+        if x.ndim != 2 or x.shape[0] != self.num_cols:
+            raise Error(f"dimension mismatch: A is {self.num_rows}x{self.num_cols}, X has shape {x.shape}")
         n = x.shape[1]
         y = out if out is not None else np.empty((self.num_rows, n), np.float32)
+        self._check_out(y, n)
         c = (cfg or KernelConfig())._c()
         _check(self.lib.spmk_spmm_host(self._h, kid.index, C.byref(c), _ptr(x, f32), n, _ptr(y, f32),
                                        C.c_void_p(stream)))
@@ -421,7 +452,10 @@ class DeviceCsr:
                         cfg: Optional[KernelConfig] = None) -> None:
         """Enqueue H2D(x) -> Y = A x -> D2H(out) on `stream` (no synchronize);
         x and out must be pinned and stay alive until the stream passes."""
-        assert x.dtype == np.float32 and x.flags.c_contiguous and out.flags.c_contiguous
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float32 and x.flags.c_contiguous and x.ndim == 2
+                and x.shape[0] == self.num_cols):
+            raise Error(f"X must be a C-contiguous float32 array of shape ({self.num_cols}, n)")
+        self._check_out(out, x.shape[1])
         c = (cfg or KernelConfig())._c()
         _check(self.lib.spmk_spmm_host_async(self._h, kid.index, C.byref(c), _ptr(x, f32), x.shape[1],
                                              _ptr(out, f32), C.c_void_p(stream)))

@@ -6,6 +6,8 @@ against the oracle for every lane width, column counts that are not multiples
 of the 32-column tile, and the tile-splitting edge cases (hub rows first,
 last, adjacent, filling a whole row-split tile, next to empty rows).
 """
+from contextlib import contextmanager
+
 import numpy as np
 import pytest
 
@@ -57,6 +59,21 @@ def hub_matrix(orc, seed=5):
     return a
 
 
+@contextmanager
+def knobs(handles, **kv):
+    """Per-handle tuning knobs (spmk_csr_set_tuning), restored afterwards."""
+    old = [{k: d.get_tuning(k) for k in kv} for d in handles]
+    for d in handles:
+        for k, v in kv.items():
+            d.set_tuning(k, v)
+    try:
+        yield
+    finally:
+        for d, o in zip(handles, old):
+            for k, v in o.items():
+                d.set_tuning(k, v)
+
+
 @pytest.fixture(scope="module")
 def cases(orc, corpus):
     sel = [a for a in corpus if a.max_row_nnz() >= 16][:4] + [hub_matrix(orc)]
@@ -64,50 +81,48 @@ def cases(orc, corpus):
 
 
 @pytest.mark.parametrize("L", [16, 100, 1000])
-def test_seq_rs_hub_rows_bit_exact(orc, cases, L, monkeypatch):
-    monkeypatch.setenv("SPMK_HUB_NNZ", str(L))
-    for a, d in cases:
-        for n in (1, 3, 32, 33, 64, 100):
-            x = orc.make_dense(a.k, n, 17 * n + L)
-            assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n} L={L}")
+def test_seq_rs_hub_rows_bit_exact(orc, cases, L):
+    with knobs([d for _, d in cases], hub_nnz=L):
+        for a, d in cases:
+            for n in (1, 3, 32, 33, 64, 100):
+                x = orc.make_dense(a.k, n, 17 * n + L)
+                assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n} L={L}")
 
 
 @pytest.mark.parametrize("W", [2, 4, 8, 16, 32, 64])
-def test_par_rs_hub_rows_bit_exact(orc, cases, W, monkeypatch):
+def test_par_rs_hub_rows_bit_exact(orc, cases, W):
     for L in (16, 300):
-        monkeypatch.setenv("SPMK_HUB_NNZ", str(L))
-        for a, d in cases:
-            for n in (1, 5, 32, 40):
-                x = orc.make_dense(a.k, n, 13 * n + W + L)
-                y = run(d, spmk.kParRowSplit, x, lane_width=W)
-                assert_bits(y, orc.spmm(a, 0, x, lane_width=W), f"{a.name} n={n} W={W} L={L}")
+        with knobs([d for _, d in cases], hub_nnz=L):
+            for a, d in cases:
+                for n in (1, 5, 32, 40):
+                    x = orc.make_dense(a.k, n, 13 * n + W + L)
+                    y = run(d, spmk.kParRowSplit, x, lane_width=W)
+                    assert_bits(y, orc.spmm(a, 0, x, lane_width=W), f"{a.name} n={n} W={W} L={L}")
 
 
-def test_hub_rows_seq_rs_tile_sizes(orc, cases, monkeypatch):
+def test_hub_rows_seq_rs_tile_sizes(orc, cases):
     """Different row-split tile sizes (rows per tile) cut differently around hubs."""
-    monkeypatch.setenv("SPMK_HUB_NNZ", "150")
     a, d = cases[-1]
     x = orc.make_dense(a.k, 8, 3)
     want = orc.spmm(a, 2, x)
     for tile in (16, 64, 256, 4096):
-        monkeypatch.setenv("SPMK_SEQ_TILE_NNZ", str(tile))
-        assert_bits(run(d, spmk.kSeqRowSplit, x), want, f"tile={tile}")
+        with knobs([d], hub_nnz=150, seq_tile_nnz=tile):
+            assert_bits(run(d, spmk.kSeqRowSplit, x), want, f"tile={tile}")
 
 
-def test_hub_path_disabled_matches(orc, cases, monkeypatch):
+def test_hub_path_disabled_matches(orc, cases):
     a, d = cases[-1]
     x = orc.make_dense(a.k, 32, 9)
-    monkeypatch.setenv("SPMK_HUB_NNZ", "0")
-    y0 = run(d, spmk.kSeqRowSplit, x)
-    monkeypatch.setenv("SPMK_HUB_NNZ", "64")
-    y1 = run(d, spmk.kSeqRowSplit, x)
+    with knobs([d], hub_nnz=0):
+        y0 = run(d, spmk.kSeqRowSplit, x)
+    with knobs([d], hub_nnz=64):
+        y1 = run(d, spmk.kSeqRowSplit, x)
     assert_bits(y1, y0, "seq-rs hub on/off")
     assert_bits(y1, orc.spmm(a, 2, x), "seq-rs vs oracle")
 
 
-def test_hub_rows_rmat_heavy(orc, monkeypatch):
+def test_hub_rows_rmat_heavy(orc):
     """Default threshold on a device R-MAT heavy graph (rows up to ~4K nonzeros)."""
-    monkeypatch.delenv("SPMK_HUB_NNZ", raising=False)
     d = spmk.DeviceCsr.generate_rmat(16, 16, SKEWS["heavy"], 1)
     h = d.download()
     a = Csr(h.num_rows, h.num_cols, np.asarray(h.row_ptr), np.asarray(h.col_idx), np.asarray(h.values), "rmat16")
@@ -119,11 +134,11 @@ def test_hub_rows_rmat_heavy(orc, monkeypatch):
 
 
 @pytest.mark.parametrize("kidx", [0, 2])
-def test_hub_path_full_corpus(orc, corpus, kidx, monkeypatch):
+def test_hub_path_full_corpus(orc, corpus, kidx):
     """Every corpus matrix with almost every row on the hub path (L = 16)."""
-    monkeypatch.setenv("SPMK_HUB_NNZ", "16")
     for a in corpus:
         d = spmk.DeviceCsr.from_host(to_host(a))
+        d.set_tuning("hub_nnz", 16)
         for n in (1, 4, 32):
             x = orc.make_dense(a.k, n, 5 * n + kidx)
             assert_bits(run(d, spmk.KernelId(kidx), x), orc.spmm(a, kidx, x), f"{a.name} n={n} k={kidx}")
@@ -135,31 +150,25 @@ def test_cfg5_hub_slice_bit_exact(orc):
     equal-nnz partition: 66M nonzeros, 51.7M of them in the 11,104 rows >= 1024 (max
     373,191), the slice the per-slice rule sends to par-rs at N=1.  The
     two-pass hub path is bit-exact against the reference order."""
-    monkeypatch_env = pytest.MonkeyPatch()
-    monkeypatch_env.delenv("SPMK_HUB_NNZ", raising=False)
-    try:
-        full = spmk.DeviceCsr.generate_rmat(25, 16, SKEWS["heavy"], 1)
-        b = full.row_slices(8)
-        d = full.slice(int(b[0]), int(b[1]))
-        del full
-        torch.cuda.empty_cache()
-        assert d.select(1) == spmk.kParRowSplit
-        h = d.download()
-        a = Csr(h.num_rows, h.num_cols, np.asarray(h.row_ptr), np.asarray(h.col_idx), np.asarray(h.values), "cfg5s0")
-        assert a.max_row_nnz() == 373191
-        x = orc.make_dense(a.k, 1, 0x00D5EED + 1)
-        assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), "cfg5 slice 0 par-rs")
-    finally:
-        monkeypatch_env.undo()
+    full = spmk.DeviceCsr.generate_rmat(25, 16, SKEWS["heavy"], 1)
+    b = full.row_slices(8)
+    d = full.slice(int(b[0]), int(b[1]))
+    del full
+    torch.cuda.empty_cache()
+    assert d.select(1) == spmk.kParRowSplit
+    h = d.download()
+    a = Csr(h.num_rows, h.num_cols, np.asarray(h.row_ptr), np.asarray(h.col_idx), np.asarray(h.values), "cfg5s0")
+    assert a.max_row_nnz() == 373191
+    x = orc.make_dense(a.k, 1, 0x00D5EED + 1)
+    assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), "cfg5 slice 0 par-rs")
 
 
-def test_seq_rs_two_pass_fold(orc, cases, monkeypatch):
+def test_seq_rs_two_pass_fold(orc, cases):
     """seq-rs through the products + streamed-fold path (one chain per column,
-    SPMK_HUB_TWO_PASS=1; off by default because the producer/folder kernel
-    is faster for seq-rs) gives the same bits."""
-    monkeypatch.setenv("SPMK_HUB_NNZ", "16")
-    monkeypatch.setenv("SPMK_HUB_TWO_PASS", "1")
-    for a, d in cases:
-        for n in (1, 3, 32, 100):
-            x = orc.make_dense(a.k, n, 11 * n)
-            assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n}")
+    hub_two_pass=1; off by default because the producer/folder kernel is
+    faster for seq-rs) gives the same bits."""
+    with knobs([d for _, d in cases], hub_nnz=16, hub_two_pass=1):
+        for a, d in cases:
+            for n in (1, 3, 32, 100):
+                x = orc.make_dense(a.k, n, 11 * n)
+                assert_bits(run(d, spmk.kSeqRowSplit, x), orc.spmm(a, 2, x), f"{a.name} n={n}")

@@ -94,19 +94,23 @@ def test_distributed_driver_single_rank_matches(graph, orc):
 
 
 @pytest.mark.parametrize("kidx", [0, 2])
-def test_graph_replay_row_split_hub_path(graph, kidx, monkeypatch):
+def test_graph_replay_row_split_hub_path(graph, kidx):
     """PageRank with a row-split kernel (what a hub-heavy slice selects) and
     most rows on the hub path: graph replay (hub kernels captured on the side
     stream) equals eager steps bit for bit."""
-    monkeypatch.setenv("SPMK_HUB_NNZ", "32")
     d, _, a, _ = graph
-    pr = prk.PageRank(d, ALPHA, kernel=spmk.KernelId(kidx))
-    x_eager, h_eager = pr.run(10, graph=False)
-    x_eager = x_eager.cpu().numpy().copy()
-    h_eager = h_eager.cpu().numpy().copy()
-    x_graph, h_graph = pr.run(10, graph=True)
-    assert np.array_equal(x_graph.cpu().numpy(), x_eager)
-    assert np.array_equal(h_graph.cpu().numpy(), h_eager)
+    old = d.get_tuning("hub_nnz")
+    d.set_tuning("hub_nnz", 32)
+    try:
+        pr = prk.PageRank(d, ALPHA, kernel=spmk.KernelId(kidx))
+        x_eager, h_eager = pr.run(10, graph=False)
+        x_eager = x_eager.cpu().numpy().copy()
+        h_eager = h_eager.cpu().numpy().copy()
+        x_graph, h_graph = pr.run(10, graph=True)
+        assert np.array_equal(x_graph.cpu().numpy(), x_eager)
+        assert np.array_equal(h_graph.cpu().numpy(), h_eager)
+    finally:
+        d.set_tuning("hub_nnz", old)
 
 
 def test_tuned_kernel_choice(graph, orc):

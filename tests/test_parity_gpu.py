@@ -202,11 +202,25 @@ def test_empty_and_degenerate_shapes():
         assert y.cpu().tolist() == [[2.0] * 4, [0.0] * 4, [3.0] * 4]
 
 
-def test_invalid_csr_rejected():
-    with pytest.raises(spmk.Error):  # unsorted columns
-        spmk.DeviceCsr.from_host(spmk.CsrMatrix(1, 4, [0, 2], [2, 1], [1.0, 1.0]))
+def test_invalid_csr_rejected(orc):
     with pytest.raises(spmk.Error):  # column out of range
         spmk.DeviceCsr.from_host(spmk.CsrMatrix(1, 2, [0, 1], [5], [1.0]))
+    with pytest.raises(spmk.Error):  # row_ptr not monotone
+        spmk.DeviceCsr.from_host(spmk.CsrMatrix(2, 2, [0, 2, 1], [0], [1.0]))
+    # Unsorted / duplicate columns: validate() rejects them (csr.hpp:95-119),
+    # spmm computes in position order like the reference's spmm_* (which never
+    # call validate), so the result equals the reference kernels' on the same arrays.
+    rp, ci = [0, 3, 5], [2, 1, 1, 0, 0]
+    va = np.array([1.5, -2.0, 0.25, 3.0, -1.0], np.float32)
+    d = spmk.DeviceCsr.from_host(spmk.CsrMatrix(2, 4, rp, ci, va))
+    with pytest.raises(spmk.Error):
+        d.validate()
+    a = Csr(2, 4, np.array(rp, np.int64), np.array(ci, np.int64), va, "unsorted")
+    for n in (1, 4):
+        x = orc.make_dense(4, n, 3 + n)
+        for kid in spmk.kAllKernels:
+            assert_bits(run(d, kid, x), orc.spmm(a, kid.index, x), f"unsorted {kid.name} n={n}")
+    spmk.DeviceCsr.from_host(spmk.CsrMatrix(1, 4, [0, 2], [1, 2], [1.0, 1.0])).validate()
 
 
 def test_determinism_and_stats(orc, dev_corpus):
@@ -283,11 +297,15 @@ def test_cfg2_full_size(orc):
 
 
 @pytest.mark.parametrize("vl", [1, 4, 8])
-def test_par_rs_virtual_lanes(orc, dev_corpus, vl, monkeypatch):
+def test_par_rs_virtual_lanes(orc, dev_corpus, vl):
     """par-rs at lane_width 32 with VL virtual lanes per physical lane (the
     tree levels inside a lane in registers): the same bits for every VL."""
-    monkeypatch.setenv("SPMK_PARRS_VL", str(vl))
     for a, d in dev_corpus:
-        for n in (1, 2, 3, 4):
-            x = orc.make_dense(a.k, n, 97 * n + vl)
-            assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), f"{a.name} n={n} vl={vl}")
+        old = d.get_tuning("parrs_vl")
+        d.set_tuning("parrs_vl", vl)
+        try:
+            for n in (1, 2, 3, 4):
+                x = orc.make_dense(a.k, n, 97 * n + vl)
+                assert_bits(run(d, spmk.kParRowSplit, x), orc.spmm(a, 0, x), f"{a.name} n={n} vl={vl}")
+        finally:
+            d.set_tuning("parrs_vl", old)
