@@ -124,27 +124,18 @@ def tuned_kernel(a: DeviceCsr, n: int, candidates: Sequence[KernelId] = kAllKern
     return best, times
 
 
-def _abs_matrix(a: DeviceCsr) -> DeviceCsr:
-    """|A| as a second resident handle (spmk_csr_abs_copy)."""
-    return a.abs_copy()
-
-
-def _abs_bound(absa: DeviceCsr, x):
-    """|A| |X| per element (the north-star tolerance scale), on the device."""
-    return absa.spmm(parse_kernel("seq-ws"), x.abs().contiguous())
-
-
 class _DevArray:
     """A borrowed device array (``__cuda_array_interface__``) for torch.as_tensor."""
 
     def __init__(self, ptr: int, n: int, typestr: str):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, True), "version": 3}
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
 
 
 def _fp64_reference(a: DeviceCsr, x):
-    """Y = A X in fp64 by an independent implementation (torch's CSR matmul
-    over the handle's arrays, values widened to double): the checker of the
-    `correct` flag, so no kernel under test judges the others."""
+    """(Y, bound) = (A X, |A| |X|) in fp64 by an independent implementation
+    (torch's CSR matmul over the handle's arrays, values widened to double):
+    the checker of the `correct` flag, so no kernel under test judges the
+    others."""
     import torch
 
     rp, ci, va = a.device_arrays()
@@ -153,7 +144,9 @@ def _fp64_reference(a: DeviceCsr, x):
     col = torch.as_tensor(_DevArray(ci, max(a.nnz, 1), "<i4"), device=dev)[: a.nnz].to(torch.int64)
     val = torch.as_tensor(_DevArray(va, max(a.nnz, 1), "<f4"), device=dev)[: a.nnz].to(torch.float64)
     m = torch.sparse_csr_tensor(row_ptr, col, val, size=(a.num_rows, a.num_cols), device=dev)
-    return m @ x.to(torch.float64)
+    am = torch.sparse_csr_tensor(row_ptr, col, val.abs(), size=(a.num_rows, a.num_cols), device=dev)
+    x64 = x.to(torch.float64)
+    return m @ x64, am @ x64.abs()
 
 
 def run_benchmark(corpus: Iterable[Tuple[str, DeviceCsr]], n_values: Sequence[int], cfg=None,
@@ -169,13 +162,11 @@ def run_benchmark(corpus: Iterable[Tuple[str, DeviceCsr]], n_values: Sequence[in
         raise Error("run_benchmark: empty corpus")
     records: List[BenchRecord] = []
     for name, a in corpus:
-        absa = _abs_matrix(a) if check else None
         for n in n_values:
             x = make_dense_device(a.num_cols, n, DENSE_SEED + n)
             ref = bound = None
             if check:
-                ref = _fp64_reference(a, x)
-                bound = _abs_bound(absa, x).to(torch.float64)
+                ref, bound = _fp64_reference(a, x)
             for kid in kAllKernels:
                 rec, y = measure_kernel(name, a, x, kid, cfg, repeats, warmup, flush_l2)
                 if check:
