@@ -88,6 +88,10 @@ class Oracle:
         L.so_kernel_tolerance.argtypes = [i64]
         L.so_kernel_tolerance.restype = f64
         L.so_oracle_rows.argtypes = [P(_SoCsr), P(f32), i64, P(i64), i64, P(f64), P(f64), C.c_int]
+        L.so_spmm_rows32.argtypes = [P(i64), P(i32), P(f32), C.c_int, i64, i64, P(f32), i64, P(i64), i64,
+                                     P(f32), C.c_int]
+        L.so_oracle_rows32.argtypes = [P(i64), P(i32), P(f32), P(f32), i64, P(i64), i64, P(f64), P(f64),
+                                       C.c_int]
 
     # -- helpers
     @staticmethod
@@ -433,3 +437,41 @@ def pagerank64(orc: Oracle, a: Csr, counts: np.ndarray, alpha: float, iters: int
         dang = x[counts == 0].sum()
         x = alpha * y + (1.0 - alpha) / m + alpha * dang / m
     return x
+
+
+def _threads(threads):
+    return threads or min(64, os.cpu_count() or 1)
+
+
+def spmm_rows(orc: "Oracle", row_ptr, col_idx32, val, kernel: int, x: np.ndarray, rows,
+              lane_width=32, seq_chunk=256, threads=None) -> np.ndarray:
+    """The reference's fp32 kernel `kernel` evaluated for the listed rows only
+    (so_spmm_rows32: same order and global chunk boundaries as the full
+    kernel).  col_idx32 is the int32 device layout; returns (len(rows), n)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx32, np.int32)
+    va = np.ascontiguousarray(val, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    rows = np.ascontiguousarray(rows, np.int64)
+    n = x.shape[1]
+    y = np.empty((len(rows), n), np.float32)
+    if orc.lib.so_spmm_rows32(_ptr(rp, i64), _ptr(ci, i32), _ptr(va, f32), kernel, lane_width, seq_chunk,
+                              _ptr(x, f32), n, _ptr(rows, i64), len(rows), _ptr(y, f32),
+                              _threads(threads)) != 0:
+        raise ValueError("invalid kernel config")
+    return y
+
+
+def oracle_rows32(orc: "Oracle", row_ptr, col_idx32, val, x: np.ndarray, rows, threads=None):
+    """fp64 ground truth and Σ|a·x| bound (csr.hpp:185-205) for listed rows, int32 columns."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx32, np.int32)
+    va = np.ascontiguousarray(val, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    rows = np.ascontiguousarray(rows, np.int64)
+    n = x.shape[1]
+    y = np.empty((len(rows), n), np.float64)
+    b = np.empty((len(rows), n), np.float64)
+    orc.lib.so_oracle_rows32(_ptr(rp, i64), _ptr(ci, i32), _ptr(va, f32), _ptr(x, f32), n, _ptr(rows, i64),
+                             len(rows), _ptr(y, f64), _ptr(b, f64), _threads(threads))
+    return y, b

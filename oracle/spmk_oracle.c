@@ -605,3 +605,202 @@ void so_oracle_rows(const so_csr* a, const float* x, int64_t n,
   oracle_worker(&jobs[0]);
   for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
 }
+
+/* ------------------------------------------------- row-subset exact kernels */
+/* The four fp32 kernels (kernels.hpp:157-464) evaluated for a list of rows
+ * only.  A row's result in every variant depends only on its own nonzeros and
+ * on where the global chunk boundaries (q*seq_chunk for seq-ws, q*lane_width
+ * for par-ws) cut it, so each listed row is recomputed here in exactly the
+ * order the full kernel uses, without touching the rest of the matrix:
+ *   par-rs  kernels.hpp:179-199  lanes restart at the row start, pairwise tree
+ *   par-ws  kernels.hpp:262-323  per chunk: rounded products, the lockstep
+ *           conditional scan (reduction.hpp:75-86) over the row's lanes only
+ *           (the scan never adds across rows), the run's last lane emitted;
+ *           complete rows store it, rows crossing chunks add the per-chunk
+ *           emissions to Y = +0 in ascending slot order (:316-323)
+ *   seq-rs  kernels.hpp:360-371  one sequential chain per column
+ *   seq-ws  kernels.hpp:410-453  per chunk a chain from +0; complete rows
+ *           store it, crossing rows add the partials to +0 in chunk order
+ * col_idx is int32 (the device layout) so full-size matrices fit host memory.
+ * tests/test_oracle.py checks this against so_spmm on the whole corpus. */
+typedef struct {
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const float* val;
+  int kernel;
+  int64_t w, chunk, n;
+  const float* x;
+  const int64_t* rows;
+  int64_t lo, hi;
+  float* y;
+} rows_job;
+
+static void row_par_rs(const rows_job* jb, int64_t s, int64_t e, float* yr, float* acc) {
+  const int64_t w = jb->w, n = jb->n;
+  for (int64_t j = 0; j < n; ++j) {
+    for (int64_t l = 0; l < w; ++l) acc[l] = 0.0f;
+    for (int64_t base = s; base < e; base += w) {
+      const int64_t lanes = (e - base) < w ? (e - base) : w;
+      for (int64_t l = 0; l < lanes; ++l) {
+        const float p = jb->val[base + l] * jb->x[(int64_t)jb->col[base + l] * n + j];
+        acc[l] += p;
+      }
+    }
+    for (int64_t len = w; len > 1; len >>= 1)
+      for (int64_t l = 0; l < len / 2; ++l) acc[l] = acc[2 * l + 1] + acc[2 * l];
+    yr[j] = acc[0];
+  }
+}
+
+static void row_par_ws(const rows_job* jb, int64_t s, int64_t e, float* yr, float* lanev) {
+  const int64_t w = jb->w, n = jb->n;
+  const int64_t q0 = s / w, q1 = (e - 1) / w;
+  for (int64_t j = 0; j < n; ++j) {
+    float out = 0.0f;
+    for (int64_t q = q0; q <= q1; ++q) {
+      const int64_t a = s > q * w ? s : q * w;
+      const int64_t b = e < (q + 1) * w ? e : (q + 1) * w;
+      const int64_t la = a - q * w, lb = b - q * w; /* run lanes [la, lb) */
+      for (int64_t l = la; l < lb; ++l)
+        lanev[l] = jb->val[q * w + l] * jb->x[(int64_t)jb->col[q * w + l] * n + j];
+      for (int64_t off = 1; off < w; off <<= 1)
+        for (int64_t i = lb - 1; i >= la + off; --i) lanev[i] += lanev[i - off];
+      const float h = lanev[lb - 1];
+      if (q0 == q1) out = h;      /* complete: stored */
+      else out += h;              /* partial slots, ascending (Y starts at +0) */
+    }
+    yr[j] = out;
+  }
+}
+
+static void row_seq(const rows_job* jb, int64_t s, int64_t e, float* yr, int ws) {
+  const int64_t n = jb->n;
+  const int64_t c = ws ? jb->chunk : (e - s + 1);
+  const int64_t q0 = ws ? s / c : 0, q1 = ws ? (e - 1) / c : 0;
+  for (int64_t j = 0; j < n; ++j) {
+    float out = 0.0f;
+    for (int64_t q = q0; q <= q1; ++q) {
+      const int64_t a = ws ? (s > q * c ? s : q * c) : s;
+      const int64_t b = ws ? (e < (q + 1) * c ? e : (q + 1) * c) : e;
+      float acc = 0.0f;
+      for (int64_t p = a; p < b; ++p) {
+        const float pr = jb->val[p] * jb->x[(int64_t)jb->col[p] * n + j];
+        acc += pr;
+      }
+      if (q0 == q1) out = acc;
+      else out += acc;
+    }
+    yr[j] = out;
+  }
+}
+
+static void* rows_worker(void* p) {
+  rows_job* jb = (rows_job*)p;
+  float* tmp = (float*)malloc(sizeof(float) * (size_t)(jb->w > 0 ? jb->w : 1));
+  for (int64_t t = jb->lo; t < jb->hi; ++t) {
+    const int64_t r = jb->rows[t];
+    const int64_t s = jb->row_ptr[r], e = jb->row_ptr[r + 1];
+    float* yr = jb->y + t * jb->n;
+    if (s == e) {
+      for (int64_t j = 0; j < jb->n; ++j) yr[j] = 0.0f;
+      continue;
+    }
+    switch (jb->kernel) {
+      case 0: row_par_rs(jb, s, e, yr, tmp); break;
+      case 1: row_par_ws(jb, s, e, yr, tmp); break;
+      case 2: row_seq(jb, s, e, yr, 0); break;
+      default: row_seq(jb, s, e, yr, 1); break;
+    }
+  }
+  free(tmp);
+  return NULL;
+}
+
+int so_spmm_rows32(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                   int kernel, int64_t lane_width, int64_t seq_chunk, const float* x,
+                   int64_t n, const int64_t* rows, int64_t count, float* y, int threads) {
+  if (so_check_config(lane_width, 0, seq_chunk) != 0) return -1;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  rows_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    rows_job* jb = &jobs[t];
+    memset(jb, 0, sizeof(*jb));
+    jb->row_ptr = row_ptr;
+    jb->col = col_idx;
+    jb->val = val;
+    jb->kernel = kernel;
+    jb->w = lane_width;
+    jb->chunk = seq_chunk;
+    jb->n = n;
+    jb->x = x;
+    jb->rows = rows;
+    jb->lo = count * t / threads;
+    jb->hi = count * (t + 1) / threads;
+    jb->y = y;
+    if (t > 0) pthread_create(&th[t], NULL, rows_worker, jb);
+  }
+  rows_worker(&jobs[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  return 0;
+}
+
+/* csr.hpp:185-205 (fp64 oracle + Σ|a·x|) for listed rows, int32 columns. */
+typedef struct {
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const float* val;
+  const float* x;
+  int64_t n;
+  const int64_t* rows;
+  int64_t lo, hi;
+  double* y;
+  double* absb;
+} oracle32_job;
+
+static void* oracle32_worker(void* p) {
+  oracle32_job* jb = (oracle32_job*)p;
+  const int64_t n = jb->n;
+  for (int64_t t = jb->lo; t < jb->hi; ++t) {
+    const int64_t i = jb->rows[t];
+    double* yr = jb->y + t * n;
+    double* br = jb->absb + t * n;
+    for (int64_t j = 0; j < n; ++j) yr[j] = br[j] = 0.0;
+    for (int64_t e = jb->row_ptr[i]; e < jb->row_ptr[i + 1]; ++e) {
+      const double v = (double)jb->val[e];
+      const float* xr = jb->x + (int64_t)jb->col[e] * n;
+      for (int64_t j = 0; j < n; ++j) {
+        const double pr = v * (double)xr[j];
+        yr[j] += pr;
+        br[j] += fabs(pr);
+      }
+    }
+  }
+  return NULL;
+}
+
+void so_oracle_rows32(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                      const float* x, int64_t n, const int64_t* rows, int64_t count,
+                      double* y, double* absbound, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  oracle32_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    oracle32_job* jb = &jobs[t];
+    jb->row_ptr = row_ptr;
+    jb->col = col_idx;
+    jb->val = val;
+    jb->x = x;
+    jb->n = n;
+    jb->rows = rows;
+    jb->lo = count * t / threads;
+    jb->hi = count * (t + 1) / threads;
+    jb->y = y;
+    jb->absb = absbound;
+    if (t > 0) pthread_create(&th[t], NULL, oracle32_worker, jb);
+  }
+  oracle32_worker(&jobs[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+}

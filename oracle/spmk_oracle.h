@@ -98,6 +98,17 @@ void so_oracle_rows(const so_csr* a, const float* x, int64_t n,
                     const int64_t* rows, int64_t count, double* y,
                     double* absbound, int threads);
 
+/* kernels.hpp:157-464 restricted to the listed rows (exact reference order,
+ * global chunk boundaries), int32 columns; y is (count x n).  Returns 0, or
+ * -1 on a bad config.  Row-parallel over `threads` pthreads. */
+int so_spmm_rows32(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                   int kernel, int64_t lane_width, int64_t seq_chunk, const float* x,
+                   int64_t n, const int64_t* rows, int64_t count, float* y, int threads);
+/* so_oracle_rows with int32 columns; y and absbound are (count x n). */
+void so_oracle_rows32(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                      const float* x, int64_t n, const int64_t* rows, int64_t count,
+                      double* y, double* absbound, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,36 @@ __device__ __forceinline__ float mul_add_rn(float acc, float v, float x) {
   return __fadd_rn(acc, __fmul_rn(v, x));
 }
 
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2).  Both lanes round to nearest like
+// the scalar ops, so results are bit-identical to __fmul_rn / __fadd_rn.
+// ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into ONE FFMA2 (one
+// rounding — not the reference's two, tools/probes/f32x2_fusion.cu), even
+// with -fmad=false, so the exact add is issued as fma(p, one, acc) with
+// `one` = {1.0f, 1.0f} passed in by the host: ptxas cannot see it is 1 and
+// cannot fold the product in, and p*1 + acc rounds once = add.rn(acc, p).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2_pack(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f32x2 r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+// {v*x.lo, v*x.hi}, each rounded (FMUL2 with a broadcast scalar operand)
+__device__ __forceinline__ f32x2 f2_mul(float v, f32x2 x) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(v, v)), "l"(x));
+  return d;
+}
+// {acc.lo + p.lo, acc.hi + p.hi}, each rounded once (FFMA2 by `one`)
+__device__ __forceinline__ f32x2 f2_add(f32x2 acc, f32x2 p, f32x2 one) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(p), "l"(one), "l"(acc));
+  return d;
+}
+constexpr f32x2 kOnePair = 0x3f8000003f800000ull;
+
 // Streaming loads for the A arrays (read once): bypass L1 allocation and mark
 // evict-first in L2 so they do not push X out of L2.
 __device__ __forceinline__ uint64_t evict_first_policy() {

@@ -140,6 +140,7 @@ void launch_seq(const SeqLaunch& l, bool ws, bool aligned, cudaStream_t s) {
   a.EXT = l.EXT;
   a.nunits = l.nunits;
   a.cvvec = ((uintptr_t)l.col % 16 == 0) && ((uintptr_t)l.val % 16 == 0);
+  a.one2 = kOnePair;
   if (ws) launch_seq_ws<true>(a, aligned, s);
   else launch_seq_ws<false>(a, aligned, s);
 }

@@ -56,6 +56,7 @@ struct SeqArgs {
   long long EXT;                 // ws: owner-extension limit (row_is_long)
   int nunits;                    // tiles
   int cvvec;                     // colIdx/val 16-byte aligned (vector batch loads)
+  f32x2 one2;                    // {1.0f, 1.0f} (kOnePair), opaque to ptxas: see f2_add
 };
 
 constexpr int kSeqThreads = 256;
@@ -311,6 +312,9 @@ seq_kernel(const SeqArgs a) {
 __device__ __forceinline__ void cp_async16(unsigned smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g));
 }
+__device__ __forceinline__ void cp_async16_hint(unsigned smem, const void* g, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem), "l"(g), "l"(pol));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int NPEND>
 __device__ __forceinline__ void cp_async_wait() {
@@ -517,28 +521,36 @@ seq_async2_kernel(const SeqArgs a) {
     issue((stage + S - 1) & (S - 1), cring[S - 1]);
     cp_async_wait<S - 1>();  // this thread's copies of batch eb have landed
     const float4* xs = ring + stage * B * NT + threadIdx.x;
-    // products off the add chain (EXACT: rounded product, kernels.hpp:439-441);
-    // fast mode keeps (v, x) and fuses them into the add
+    // products off the add chain (EXACT: rounded product, kernels.hpp:439-441,
+    // as FMUL2 pairs); fast mode keeps (v, x) and fuses them into the add
     float pv[B], px[B][4];
+    f32x2 pp[B][2];
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const float v = gshfl<LPU>(vring[0][j / LPU], j % LPU);
       const float4 x = xs[j * NT];
       if constexpr (EXACT) {
-        px[j][0] = __fmul_rn(v, x.x);
-        px[j][1] = __fmul_rn(v, x.y);
-        px[j][2] = __fmul_rn(v, x.z);
-        px[j][3] = __fmul_rn(v, x.w);
+        pp[j][0] = f2_mul(v, f2_pack(x.x, x.y));
+        pp[j][1] = f2_mul(v, f2_pack(x.z, x.w));
       } else {
         px[j][0] = x.x; px[j][1] = x.y; px[j][2] = x.z; px[j][3] = x.w;
       }
       pv[j] = v;
     }
-    auto next_bit = [&](int from) -> unsigned {
+    // positions holding some unit's next event: with B <= LPU lane gl of a
+    // unit votes for position gl and the units' bytes are folded, else REDUX
+    auto next_bits = [&](int from) -> unsigned {
       const int d = st.nev - eb;
-      return (st.live && d >= from && d < B) ? (1u << d) : 0u;
+      if constexpr (B <= LPU) {
+        unsigned m = __ballot_sync(FULL, st.live && d == st.gl && d >= from);
+        if constexpr (LPU < 32) m |= m >> 16;
+        if constexpr (LPU < 16) m |= m >> 8;
+        return m & ((1u << B) - 1u);
+      } else {
+        return __reduce_or_sync(FULL, (st.live && d >= from && d < B) ? (1u << d) : 0u);
+      }
     };
-    unsigned wm = __reduce_or_sync(FULL, next_bit(0));
+    unsigned wm = next_bits(0);
     // unrolled positions; a warp-uniform branch into the event handler only
     // where some unit has an event (measured 9 % faster than add rounds
     // between events: cfg2 320 -> 290 us)
@@ -546,11 +558,18 @@ seq_async2_kernel(const SeqArgs a) {
     for (int j = 0; j < B; ++j) {
       if (wm & (1u << j)) {
         if (st.live && st.nev == eb + j) st.event(a, eb + j);
-        wm = __reduce_or_sync(FULL, next_bit(j + 1));
+        wm = next_bits(j + 1);
       }
+      if constexpr (EXACT) {
+        // acc += product, FFMA2 by one (two roundings in all: FMUL2 above, this)
+        f32x2 a01 = f2_add(f2_pack(st.acc[0], st.acc[1]), pp[j][0], a.one2);
+        f32x2 a23 = f2_add(f2_pack(st.acc[2], st.acc[3]), pp[j][1], a.one2);
+        f2_unpack(a01, st.acc[0], st.acc[1]);
+        f2_unpack(a23, st.acc[2], st.acc[3]);
+      } else {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        st.acc[k] = EXACT ? __fadd_rn(st.acc[k], px[j][k]) : fmaf(pv[j], px[j][k], st.acc[k]);
+        for (int k = 0; k < 4; ++k) st.acc[k] = fmaf(pv[j], px[j][k], st.acc[k]);
+      }
     }
     stage = (stage + 1) & (S - 1);
 #pragma unroll

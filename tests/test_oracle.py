@@ -180,3 +180,41 @@ def test_reference_kats_selector(orc):
     assert orc.select_kernel(64, 0.5, 2) == 0
     assert orc.select_kernel(32.0, 0.5, 1) == 0  # ties favor row-split
     assert orc.select_kernel(10.0, 1.0, 32) == 2
+
+
+# ---------------------------------------------------------------- row-subset mode
+def test_row_subset_oracle_matches_full_kernels(orc, corpus):
+    """so_spmm_rows32 (used at full BASELINE size, where the whole-matrix
+    restatement is too slow) reproduces so_spmm row for row: every variant,
+    lane widths 2..64, seq_chunk 1..4096, rows in shuffled order."""
+    from oracle.oracle import oracle_rows32, spmm_rows
+
+    rng = np.random.default_rng(3)
+    for a in corpus[::2]:
+        rows = rng.permutation(a.m)[: max(1, a.m // 2)]
+        col32 = a.col_idx.astype(np.int32)
+        for n in (1, 3, 8):
+            x = orc.make_dense(a.k, n, 11 + n)
+            for kidx in range(4):
+                for W, S in ((32, 256), (2, 1), (64, 7), (8, 4096), (16, 33)):
+                    full = orc.spmm(a, kidx, x, lane_width=W, seq_chunk=S)[rows]
+                    sub = spmm_rows(orc, a.row_ptr, col32, a.val, kidx, x, rows, lane_width=W, seq_chunk=S,
+                                    threads=3)
+                    assert np.array_equal(full.view(np.uint32), sub.view(np.uint32)), (a.name, n, kidx, W, S)
+        y, b = oracle_rows32(orc, a.row_ptr, col32, a.val, x, rows, threads=2)
+        y2, b2 = orc.oracle_rows(a, x, rows=rows, threads=2)
+        assert np.array_equal(y, y2) and np.array_equal(b, b2)
+
+
+def test_row_subset_oracle_against_reference(orc, ref, corpus):
+    from oracle.oracle import spmm_rows
+
+    for a in corpus[1::5]:
+        h = ref.handle(a)
+        rows = np.arange(a.m)[::-3]
+        x = orc.make_dense(a.k, 5, 21)
+        for kidx in range(4):
+            yr = h.spmm(kidx, x, lane_width=16, seq_chunk=100)[rows]
+            ys = spmm_rows(orc, a.row_ptr, a.col_idx.astype(np.int32), a.val, kidx, x, rows, lane_width=16,
+                           seq_chunk=100)
+            assert np.array_equal(yr.view(np.uint32), ys.view(np.uint32)), (a.name, kidx)
