@@ -36,7 +36,7 @@ typedef enum {
   SPMK_EDIM = 2,         /* dimension mismatch (kernels.hpp:103-109)         */
   SPMK_ECUDA = 3,        /* CUDA runtime error                               */
   SPMK_ENOMEM = 4,       /* device allocation failed                         */
-  SPMK_ENCCL = 5,        /* reserved: collective failure                     */
+  SPMK_ENCCL = 5,        /* NCCL missing or a collective failed (spmk_mg_*)  */
   SPMK_EUNSUPPORTED = 6  /* valid for the reference, not on this device path */
 } spmk_status;
 
@@ -278,6 +278,63 @@ spmk_status spmk_ipc_handle(const void* d_ptr, void* handle64);
 spmk_status spmk_ipc_open(const void* handle64, void** d_ptr);
 spmk_status spmk_ipc_close(void* d_ptr);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* One process (or thread) per GPU over NCCL (NVLink 5 / NVSwitch), for the
+ * row-partitioned configs.  Replaces the reference's
+ * single-process parallel substrate (ThreadPool, thread_pool.hpp:51-76, whose
+ * static partition kernels.hpp:124-129 is applied here to nonzeros): A is cut
+ * into equal-nnz row slices (spmk_row_slices), X is replicated once, every
+ * rank computes its own Y slice with the per-slice rule — no collective in
+ * the SpMM — and only the iterative driver exchanges Y.  NCCL is loaded at
+ * run time (libnccl.so.2); without it these calls return SPMK_ENCCL and the
+ * rest of the library is unaffected.  Collectives are enqueued on `stream`
+ * (asynchronous) and must be issued in the same order on every rank. */
+typedef struct spmk_mg_s* spmk_mg_t;
+#define SPMK_MG_UNIQUE_ID_BYTES 128
+/* NCCL present?  nccl_version (may be NULL) receives ncclGetVersion. */
+spmk_status spmk_mg_available(int* nccl_version);
+/* Rank 0 creates the id and ships it to the others out of band. */
+spmk_status spmk_mg_unique_id(void* id128);
+/* Collective over all ranks (ncclCommInitRank), bound to `device`. */
+spmk_status spmk_mg_init(const void* id128, int nranks, int rank, int device,
+                         spmk_mg_t* out);
+spmk_status spmk_mg_destroy(spmk_mg_t mg);
+spmk_status spmk_mg_info(spmk_mg_t mg, int* rank, int* nranks, int* device);
+/* This rank's equal-nnz row slice of `full` (bounds = spmk_row_slices(full,
+ * nranks)) as a rebased handle on the communicator's device; row_begin /
+ * row_end (may be NULL) receive its global rows. */
+spmk_status spmk_mg_slice(spmk_mg_t mg, spmk_csr_t full, spmk_csr_t* slice,
+                          int64_t* row_begin, int64_t* row_end);
+/* In-place broadcast of `count` floats from `root` (X replication). */
+spmk_status spmk_mg_broadcast(spmk_mg_t mg, float* d_buf, int64_t count,
+                              int root, void* stream);
+/* In-place all-gather of X cut into nranks equal chunks of `chunk` floats
+ * (rank g owns d_x[g*chunk, (g+1)*chunk)): each rank uploads 1/nranks of a
+ * host X over its own PCIe link, NVLink assembles the rest.  d_x holds
+ * nranks*chunk floats (pad the tail). */
+spmk_status spmk_mg_allgather_x(spmk_mg_t mg, float* d_x, int64_t chunk,
+                                void* stream);
+/* Y exchange of the iterative driver: rank g's rows
+ * [row_bounds[g], row_bounds[g+1]) of the row-major (rows x n) d_y are
+ * broadcast from g to all ranks, in place, as ONE NCCL group (unequal
+ * slices: no padded all-gather).  row_bounds is a HOST array of nranks+1. */
+spmk_status spmk_mg_allgather_rows(spmk_mg_t mg, float* d_y,
+                                   const int64_t* row_bounds, int64_t n,
+                                   void* stream);
+/* In-place sum all-reduces (PageRank residual / dangling mass; counts). */
+spmk_status spmk_mg_allreduce_f64(spmk_mg_t mg, double* d_buf, int64_t count,
+                                  void* stream);
+spmk_status spmk_mg_allreduce_i32(spmk_mg_t mg, int32_t* d_buf, int64_t count,
+                                  void* stream);
+/* Device barrier (a 4-byte all-reduce), then synchronizes `stream`. */
+spmk_status spmk_mg_barrier(spmk_mg_t mg, void* stream);
+/* This rank's SpMM: spmk_spmm_auto on its slice (per-slice features and
+ * rule); no collective — X must already be replicated. */
+spmk_status spmk_mg_spmm(spmk_mg_t mg, spmk_csr_t slice, const spmk_thresholds* t,
+                         const spmk_kernel_config* cfg, const float* d_x,
+                         int64_t n, float* d_y, void* stream,
+                         spmk_kernel_id* chosen);
+
 /* ------------------------------------------------------------ generators */
 /* generate_rmat<float> (rmat.hpp:61-88 + csr.hpp:123-164) on the device,
  * bit-identical to the reference (counter form of SplitMix64): returns a
@@ -288,6 +345,22 @@ spmk_status spmk_generate_rmat(uint32_t scale, uint64_t edge_factor, double a,
 /* make_dense<float> (corpus.hpp:116-122) on the device: d_out[rows*cols]. */
 spmk_status spmk_make_dense(int64_t rows, int64_t cols, uint64_t seed,
                             float* d_out, void* stream);
+/* The same into HOST memory (generated on `device`, copied back). */
+spmk_status spmk_make_dense_host(int64_t rows, int64_t cols, uint64_t seed,
+                                 float* out, int device);
+
+/* ------------------------------------------------------------ harness */
+/* measure_kernel (bench.hpp:65-98) on the device: X = make_dense(num_cols, n,
+ * x_seed) in HBM, `warmup` untimed calls, then `repeats` calls each bracketed
+ * by CUDA events (a 256 MiB buffer written before each when flush_l2), median
+ * seconds; `correct` (may be NULL) = matches_oracle (bench.hpp:47-58): every
+ * |y - o| <= kernel_tolerance(max_row_nnz) * max(1, |o|) against the fp64
+ * product o computed by an independent row-parallel device kernel. */
+spmk_status spmk_measure_kernel(spmk_csr_t a, spmk_kernel_id id,
+                                const spmk_kernel_config* cfg, int64_t n,
+                                uint64_t x_seed, int64_t repeats, int64_t warmup,
+                                int flush_l2, double* median_seconds,
+                                int* correct);
 
 #ifdef __cplusplus
 }

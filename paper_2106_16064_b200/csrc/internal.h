@@ -8,6 +8,7 @@
 //   launch_par.cu   par-rs / par-ws / hub-row kernels (par_*.cuh, hub_kernels.cuh)
 //   capi_gen.cu     device generators (gen_kernels.cuh)
 //   capi_iter.cu    iterative SpMV / PageRank support + CUDA IPC (iter_kernels.cuh)
+//   capi_bench.cu   selection-harness measurement (spmk_measure_kernel) + host make_dense
 //   capi_mg.cu      multi-GPU layer over NCCL (spmk_mg_*)
 //
 // Every kernel header is included by exactly one translation unit (they define

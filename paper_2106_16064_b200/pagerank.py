@@ -154,19 +154,6 @@ class PageRank:
 
 
 # --------------------------------------------------------------------- multi-GPU
-def exchange_slices(x, bounds: List[int], group=None) -> None:
-    """Every rank holds x (length bounds[-1]) with its own slice
-    x[bounds[r]:bounds[r+1]] up to date; after this call all slices are
-    everywhere.  One broadcast per rank (unequal slices, no padding)."""
-    import torch.distributed as dist
-
-    for g in range(len(bounds) - 1):
-        lo, hi = int(bounds[g]), int(bounds[g + 1])
-        if hi > lo:
-            src = g if group is None else dist.get_global_rank(group, g)  # src is a global rank
-            dist.broadcast(x[lo:hi], src=src, group=group)
-
-
 def _ipc_handle(t) -> bytes:
     buf = (C.c_char * 64)()
     _check(_lib().spmk_ipc_handle(vp(t.data_ptr()), C.cast(buf, vp)))
@@ -184,20 +171,27 @@ class DistributedPageRank:
     """One rank of the row-partitioned iterative SpMV.  ``full`` is the whole
     square A on this rank's GPU (each rank keeps only its slice afterwards).
 
-    exchange="nccl": update this rank's slice of x in place, then one NCCL
-    broadcast per rank (unequal slices).  exchange="p2p": x is double-buffered
+    Collectives go through the library's NCCL layer (``multigpu.Communicator``,
+    spmk_mg_*): the global out-degree and (residual, dangling) all-reduces, and
+    for exchange="nccl" the Y exchange — update this rank's slice of x in
+    place, then spmk_mg_allgather_rows (one grouped broadcast per rank's
+    unequal slice).  exchange="p2p": x is double-buffered
     and every rank's update kernel stores its slice of x_next straight into
     all ranks' replicas (CUDA-IPC-mapped peer buffers, P2P over NVLink) —
     update and all-gather fused into one kernel; the residual all-reduce that
     follows is the barrier before the next SpMV reads x_next."""
 
-    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None, exchange: str = "nccl", kernel=None):
+    def __init__(self, full: DeviceCsr, alpha: float = 0.85, group=None, exchange: str = "nccl", kernel=None,
+                 comm=None):
         import torch
         import torch.distributed as dist
 
+        from .multigpu import Communicator
+
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
-        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.comm = comm if comm is not None else Communicator.from_torch_distributed(group)
+        self.rank, self.world = self.comm.rank, self.comm.world
         self.group, self.alpha, self.m, self.exchange = group, float(alpha), full.num_rows, exchange
         dev = torch.cuda.current_device()
         self.bounds = [int(b) for b in full.row_slices(self.world)]
@@ -205,7 +199,7 @@ class DistributedPageRank:
         self.lo, self.hi = lo, hi
         self.a = full.slice(lo, hi, device=dev)
         counts = column_counts(self.a)
-        dist.all_reduce(counts, group=group)  # global out-degrees (integer: exact)
+        self.comm.allreduce(counts)  # global out-degrees (integer: exact)
         self.counts = counts
         make_column_stochastic(self.a, counts)
         # per-slice choice: the rule on this slice's features (None), "tuned"
@@ -253,10 +247,8 @@ class DistributedPageRank:
         self.opened = []
 
     def _global_base(self):
-        import torch.distributed as dist
-
         red = self.state[1:3].clone()
-        dist.all_reduce(red, group=self.group)
+        self.comm.allreduce(red)
         self.state[1:3] = red
         self.state[0] = (1.0 - self.alpha) / self.m + self.alpha * red[1] / self.m
 
@@ -300,7 +292,7 @@ class DistributedPageRank:
                                          C.c_double(self.alpha), vp(self.state.data_ptr()),
                                          vp(self.scratch.data_ptr()), vp(0), 0, vp(st.cuda_stream)))
         self._global_base()
-        exchange_slices(x.view(-1), self.bounds, self.group)
+        self.comm.allgather_rows(x, self.bounds, 1)
 
     def run(self, iters: int = 50):
         self.reset()

@@ -94,8 +94,23 @@ _SIGS = {
     "spmk_launch_count": ([], u64),
     "spmk_timing_enable": ([C.c_int], C.c_int),
     "spmk_timing_last": ([P(f32), P(f32)], C.c_int),
+    "spmk_mg_available": ([P(C.c_int)], C.c_int),
+    "spmk_mg_unique_id": ([vp], C.c_int),
+    "spmk_mg_init": ([vp, C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
+    "spmk_mg_destroy": ([vp], C.c_int),
+    "spmk_mg_info": ([vp, P(C.c_int), P(C.c_int), P(C.c_int)], C.c_int),
+    "spmk_mg_slice": ([vp, vp, P(vp), P(i64), P(i64)], C.c_int),
+    "spmk_mg_broadcast": ([vp, vp, i64, C.c_int, vp], C.c_int),
+    "spmk_mg_allgather_x": ([vp, vp, i64, vp], C.c_int),
+    "spmk_mg_allgather_rows": ([vp, vp, P(i64), i64, vp], C.c_int),
+    "spmk_mg_allreduce_f64": ([vp, vp, i64, vp], C.c_int),
+    "spmk_mg_allreduce_i32": ([vp, vp, i64, vp], C.c_int),
+    "spmk_mg_barrier": ([vp, vp], C.c_int),
+    "spmk_mg_spmm": ([vp, vp, P(_Thr), P(_Cfg), vp, i64, vp, vp, P(C.c_int)], C.c_int),
     "spmk_generate_rmat": ([C.c_uint32, u64, f64, f64, f64, f64, u64, C.c_int, P(vp)], C.c_int),
     "spmk_make_dense": ([i64, i64, u64, vp, vp], C.c_int),
+    "spmk_make_dense_host": ([i64, i64, u64, P(f32), C.c_int], C.c_int),
+    "spmk_measure_kernel": ([vp, C.c_int, P(_Cfg), i64, u64, i64, i64, C.c_int, P(f64), P(C.c_int)], C.c_int),
     "spmk_column_counts": ([vp, vp, vp], C.c_int),
     "spmk_csr_values_inv_column_counts": ([vp, vp, vp], C.c_int),
     "spmk_pagerank_scratch_doubles": ([], i64),
