@@ -25,7 +25,7 @@ DenseMatrix<T> make_dense(Index rows, Index cols, std::uint64_t seed) {
   static_assert(std::is_same_v<T, float>, "spmk (B200): make_dense is fp32 only");
   if (rows < 0 || cols < 0) throw Error("negative dimension");
   DenseMatrix<T> x = DenseMatrix<T>::zero(rows, cols);
-  detail::check_status(spmk_make_dense_host(rows, cols, seed, x.data.data(), detail::current_device()),
+  detail::check_status(spmk_make_dense_host(rows, cols, seed, x.data.data(), current_device()),
                        "make_dense");
   return x;
 }

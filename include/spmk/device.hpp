@@ -45,6 +45,18 @@ class DeviceCsr {
   }
 
   spmk_csr_t handle() const { return h_; }
+  // Back to the reference's host layout (int64 indices).
+  CsrMatrix<float> download() const {
+    const Info i = info();
+    CsrMatrix<float> a;
+    a.num_rows = i.num_rows;
+    a.num_cols = i.num_cols;
+    a.row_ptr.assign(static_cast<std::size_t>(i.num_rows) + 1, 0);
+    a.col_idx.assign(static_cast<std::size_t>(i.nnz), 0);
+    a.values.assign(static_cast<std::size_t>(i.nnz), 0.f);
+    detail::check_status(spmk_csr_download(h_, a.row_ptr.data(), a.col_idx.data(), a.values.data()), "download");
+    return a;
+  }
   Index num_rows() const { return info().num_rows; }
   Index num_cols() const { return info().num_cols; }
   Index nnz() const { return info().nnz; }

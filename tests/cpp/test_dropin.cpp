@@ -5,6 +5,8 @@
 //
 //   ./test_dropin          every case (needs a GPU)
 //   ./test_dropin --host   host-only cases (selector, config, names, plan)
+#include <array>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -58,7 +60,7 @@ struct Reg {
 
 // make_dense (corpus.hpp:116-122): element i = float(2u-1), u the (i+1)-th
 // SplitMix64 unit draw of `seed`.
-DenseMatrix<float> make_dense(Index rows, Index cols, std::uint64_t seed) {
+DenseMatrix<float> host_make_dense(Index rows, Index cols, std::uint64_t seed) {
   DenseMatrix<float> d = DenseMatrix<float>::zero(rows, cols);
   for (std::size_t i = 0; i < d.data.size(); ++i) {
     std::uint64_t z = seed + (i + 1) * 0x9e3779b97f4a7c15ULL;
@@ -88,9 +90,116 @@ MatrixFeatures feats(double avg, double cv, Index rows = 1000) {
   return f;
 }
 
+// test_bench.cpp helpers: a 32x32 random corpus (SplitMix64 rmat.hpp:15-29)
+struct Mix {
+  std::uint64_t s;
+  std::uint64_t next() {
+    std::uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  double unit() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+std::vector<NamedMatrix<float>> tiny_corpus() {
+  std::vector<Triple<float>> t;
+  Mix rng{1};
+  for (int i = 0; i < 200; ++i) {
+    const Index r = Index(rng.next() % 32), c = Index(rng.next() % 32);
+    t.push_back({r, c, static_cast<float>(2.0 * rng.unit() - 1.0)});
+  }
+  std::vector<NamedMatrix<float>> corpus;
+  corpus.emplace_back("tiny", csr_from_coo(std::move(t), 32, 32));
+  return corpus;
+}
+BenchRecord make_record(const std::string& m, std::size_t n, KernelId k, double g, bool a) {
+  BenchRecord r;
+  r.matrix_name = m;
+  r.nnz = 100;
+  r.n = n;
+  r.kernel = kernel_name(k);
+  r.gflops = g;
+  r.time_seconds = 2.0 * 100 * double(n) / g / 1e9;
+  r.selected_by_rule = a;
+  return r;
+}
+void add_cell(std::vector<BenchRecord>& rec, const std::string& m, std::size_t n, std::array<double, 4> g,
+              KernelId chosen) {
+  for (std::size_t k = 0; k < 4; ++k) rec.push_back(make_record(m, n, kAllKernels[k], g[k], false));
+  rec.push_back(make_record(m, n, chosen, g[kernel_index(chosen)], true));
+}
+bool near(double a, double b, double eps = 1e-9) { return std::fabs(a - b) <= eps * std::max(1.0, std::fabs(b)); }
+
 }  // namespace
 
 // ------------------------------------------------------------- host-only
+TEST_CASE("summarize: auto matching best gives zero loss (test_bench.cpp:87-95)", false) {
+  std::vector<BenchRecord> r;
+  add_cell(r, "m1", 1, {1, 2, 3, 4}, kSeqBalanced);
+  add_cell(r, "m1", 8, {5, 2, 3, 4}, kParRowSplit);
+  auto s = summarize_selection_loss(r);
+  CHECK(near(s.per_n_loss.at(1), 0.0) && near(s.per_n_loss.at(8), 0.0));
+  CHECK(near(s.single_kernel_loss.at("seq-ws"), 0.1));
+}
+
+TEST_CASE("summarize: half the best, shifting landscape, fixed-kernel loss (test_bench.cpp:97-135)", false) {
+  std::vector<BenchRecord> r;
+  add_cell(r, "m1", 4, {2, 4, 1, 1}, kParRowSplit);
+  add_cell(r, "m2", 4, {3, 6, 1, 1}, kParRowSplit);
+  CHECK(near(summarize_selection_loss(r).per_n_loss.at(4), 0.5));
+  r.clear();
+  for (int m = 0; m < 4; ++m) {
+    const std::string name = "m" + std::to_string(m);
+    add_cell(r, name, 1, {10, 9, 2, 2}, kParRowSplit);
+    add_cell(r, name, 4, {9, 10, 2, 2}, kParBalanced);
+    add_cell(r, name, 32, {2, 2, 10, 9}, kSeqRowSplit);
+    add_cell(r, name, 128, {2, 2, 9, 10}, kSeqBalanced);
+  }
+  auto s = summarize_selection_loss(r);
+  for (const auto& [k, l] : s.single_kernel_loss) CHECK(mean_per_n_loss(s) < l);
+  CHECK(min_single_kernel_loss(s) > 0.0);
+  r.clear();
+  add_cell(r, "m1", 2, {5, 1, 1, 1}, kParRowSplit);
+  add_cell(r, "m1", 16, {5, 1, 1, 1}, kSeqRowSplit);
+  s = summarize_selection_loss(r);
+  CHECK(s.single_kernel_loss.at("par-rs") == 0.0 && s.single_kernel_loss.at("par-ws") > 0.0);
+}
+
+TEST_CASE("summarize rejects incomplete record sets; emit_csv shapes (test_bench.cpp:137-175)", false) {
+  std::vector<BenchRecord> r;
+  add_cell(r, "m1", 1, {1, 2, 3, 4}, kSeqBalanced);
+  r.pop_back();
+  CHECK_THROWS_AS(summarize_selection_loss(r), Error);
+  r.clear();
+  add_cell(r, "m1", 1, {1, 2, 3, 4}, kSeqBalanced);
+  r.erase(r.begin());
+  CHECK_THROWS_AS(summarize_selection_loss(r), Error);
+  std::ostringstream out;
+  emit_csv({}, SelectionLossSummary{}, out);
+  CHECK(out.str() == "matrix_name,num_rows,num_cols,nnz,n,kernel,time_seconds,gflops,correct,selected_by_rule\n");
+  r.clear();
+  add_cell(r, "m1", 1, {1, 2, 3, 4}, kSeqBalanced);
+  std::ostringstream out2;
+  emit_csv(r, summarize_selection_loss(r), out2);
+  std::istringstream lines(out2.str());
+  std::string line;
+  int data = 0, comments = 0;
+  std::getline(lines, line);
+  while (std::getline(lines, line)) (line[0] == '#' ? comments : data) += 1;
+  CHECK(data == 5 && comments == 5);
+}
+
+TEST_CASE("rmat params validation (test_rmat.cpp)", false) {
+  RmatParams p;
+  p.scale = 0;
+  CHECK_THROWS_AS(validate(p), Error);
+  p.scale = 8;
+  p.edge_factor = 0;
+  CHECK_THROWS_AS(validate(p), Error);
+  p.edge_factor = 8;
+  p.skew = RmatSkew{0.5, 0.5, 0.5, 0.0};
+  CHECK_THROWS_AS(validate(p), Error);
+}
 TEST_CASE("kernel names, indices and parse round trip (kernels.hpp:40-57)", false) {
   const char* names[] = {"par-rs", "par-ws", "seq-rs", "seq-ws"};
   for (std::size_t i = 0; i < 4; ++i) {
@@ -253,7 +362,7 @@ TEST_CASE("identity passes X through bit-exactly (test_kernels.cpp:89-99)", true
   std::vector<Triple<float>> t;
   for (Index i = 0; i < 4; ++i) t.push_back({i, i, 1.f});
   auto a = csr_from_coo(std::move(t), 4, 4);
-  auto x = make_dense(4, 8, 17);
+  auto x = host_make_dense(4, 8, 17);
   for (KernelId id : kAllKernels) CHECK(spmm(id, a, x).data == x.data);
 }
 
@@ -301,7 +410,7 @@ TEST_CASE("lane-multiply counters (test_kernels.cpp:248-272)", true) {
     for (Index j = 0; j < len; ++j) t.push_back({i, (i + 13 * j) % 200, 1.f});
   }
   auto a = csr_from_coo(std::move(t), 200, 200);
-  auto x = make_dense(200, 1, 77);
+  auto x = host_make_dense(200, 1, 77);
   KernelStats bal, rs;
   KernelConfig cfg;
   cfg.stats = &bal;
@@ -318,10 +427,47 @@ TEST_CASE("resident handle: device R-MAT, features, rule, both call shapes agree
   const KernelId k = d.select(32);
   const MatrixFeatures f = d.features();
   CHECK(select_kernel(f, 32) == k);
-  auto x = make_dense(d.num_cols(), 32, 0x00D5EED + 32);
+  auto x = host_make_dense(d.num_cols(), 32, 0x00D5EED + 32);
   auto y1 = d.spmm(k, x);
   auto y2 = d.spmm(k, x);
   CHECK(y1.data == y2.data);
+}
+
+TEST_CASE("generate_rmat<float> and make_dense<float> on the device (rmat.hpp:61-88, corpus.hpp:116-122)", true) {
+  RmatParams p;
+  p.scale = 10;
+  p.edge_factor = 8;
+  p.seed = 7;
+  const CsrMatrix<float> a = generate_rmat<float>(p);
+  validate(a);
+  CHECK(a.num_rows == 1024 && a.nnz() > 0);
+  const CsrMatrix<float> b = DeviceCsr::rmat(10, 8, 0.57, 0.19, 0.19, 0.05, 7).download();
+  CHECK(a.row_ptr == b.row_ptr && a.col_idx == b.col_idx && a.values == b.values);
+  for (float v : a.values) CHECK(v == 1.0f);
+  const auto x = make_dense<float>(1000, 7, 17);
+  const auto h = host_make_dense(1000, 7, 17);
+  CHECK(x.num_rows == 1000 && x.num_cols == 7 && x.data == h.data);
+}
+
+TEST_CASE("run_benchmark: records, correctness, gflops, the auto record (test_bench.cpp:56-85)", true) {
+  auto records = run_benchmark(tiny_corpus(), {1}, {}, {}, 3, 0);
+  CHECK(records.size() == 5);
+  int autos = 0;
+  for (const auto& r : records) {
+    CHECK(r.correct && r.time_seconds > 0.0);
+    CHECK(near(r.gflops, 2.0 * double(r.nnz) * double(r.n) / r.time_seconds / 1e9));
+    autos += r.selected_by_rule;
+  }
+  CHECK(autos == 1);
+  auto corpus = tiny_corpus();
+  records = run_benchmark(corpus, {1, 8}, {}, {}, 2, 0);
+  const auto f = extract_features(corpus[0].second);
+  for (const auto& r : records)
+    if (r.selected_by_rule) CHECK(r.kernel == kernel_name(select_kernel(f, r.n)));
+  auto s = summarize_selection_loss(records);
+  CHECK(s.per_n_loss.size() == 2);
+  CHECK_THROWS_AS(run_benchmark<float>({}, {1}, {}, {}, 1, 0), Error);
+  CHECK_THROWS_AS(run_benchmark(tiny_corpus(), {1}, {}, {}, 0, 0), Error);
 }
 
 int main(int argc, char** argv) {
