@@ -133,8 +133,6 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     return SPMK_OK;
   }
   if (n > INT32_MAX / 2) return fail(SPMK_EUNSUPPORTED, "n too large");
-  if (id == SPMK_PAR_BALANCED && cfg.lane_width > 32)
-    return fail(SPMK_EUNSUPPORTED, "par-ws with lane_width 64 is not supported on the device");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CK(cudaStreamIsCapturing(s, &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
@@ -223,6 +221,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       a.hub = hubs ? L : INT32_MAX;
       timing_record(1, s);
       launch_par_rs(a, W, par_rs_vl(h, W, N), aligned, s);
+      timing_record(2, s);
+    } else if (W == 64) {
+      const long long nch = (h->nnz + 63) / 64;
+      float* slots = h->scratch.get((size_t)(2 * nch) * N);
+      timing_record(1, s);
+      launch_par_ws64(a, slots, s);
       timing_record(2, s);
     } else {
       // T chunks of W nonzeros per tile (4 or 8: the two compiled shapes)

@@ -12,6 +12,7 @@
 #include "internal.h"
 #include "par_kernels.cuh"
 #include "par_ws.cuh"
+#include "par_ws64.cuh"
 
 using namespace spmk_dev;
 
@@ -186,6 +187,13 @@ void launch_par_ws(const ParLaunch& l, int W, int T, bool aligned, cudaStream_t 
   const ParArgs a = to_args(l);
   if (T == 8) launch_par_ws_tt<8, 4>(a, W, aligned, s);
   else launch_par_ws_tt<4, 5>(a, W, aligned, s);
+}
+
+void launch_par_ws64(const ParLaunch& l, float* slots, cudaStream_t s) {
+  ParWs64Args a{l.crp, l.rid, l.col, l.val, l.X, l.Y, slots, l.mne, l.nnz, l.N, ((long long)l.nnz + 63) / 64};
+  par_ws64_chunk_kernel<<<grid_for(a.chunks * 32, 256, 148 * 64), 256, 0, s>>>(a); LAUNCHED(1);
+  par_ws64_merge_kernel<<<grid_for((long long)a.mne * a.N), 256, 0, s>>>(a); LAUNCHED(1);
+  CK(cudaGetLastError());
 }
 
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, int L, const float* d_x, int N,

@@ -70,8 +70,8 @@ def test_error_paths(mat):
         mat.spmm(spmk.kSeqBalanced, x)  # dimension mismatch
     with pytest.raises(spmk.Error):
         spmk.check_config(spmk.KernelConfig(lane_width=3))
-    with pytest.raises(spmk.UnsupportedError):
+    with pytest.raises(spmk.Error):
         mat.spmm(spmk.kParBalanced, torch.randn(mat.num_cols, 4, device="cuda"),
-                 cfg=spmk.KernelConfig(lane_width=64))
+                 cfg=spmk.KernelConfig(lane_width=128))
     with pytest.raises(spmk.Error):
         spmk.DeviceCsr.generate_rmat(0, 8)

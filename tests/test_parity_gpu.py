@@ -137,11 +137,7 @@ def test_lane_width_variants(orc, dev_corpus, W):
     for a, d in dev_corpus[::2]:
         for n in (1, 3, 4, 8, 32):
             x = orc.make_dense(a.k, n, 31 * n + W)
-            for kidx in (0, 1):
-                if kidx == 1 and W == 64:
-                    with pytest.raises(spmk.UnsupportedError):
-                        run(d, spmk.KernelId(1), x, lane_width=64)
-                    continue
+            for kidx in (0, 1):  # par-ws at W=64: par_ws64.cuh (two virtual lanes per lane)
                 y = run(d, spmk.KernelId(kidx), x, lane_width=W)
                 assert_bits(y, orc.spmm(a, kidx, x, lane_width=W), f"{a.name} n={n} k={kidx} W={W}")
 
