@@ -127,6 +127,17 @@ __global__ void compact_scatter_kernel(const int* __restrict__ rp, int m,
   }
 }
 
+// Segment heads of the 32-nonzero chunks: bit (p & 31) of word p >> 5 for
+// every row start p = crp[r] (non-empty rows, so distinct positions), plus a
+// phantom head at p = nnz = crp[mne] closing the last row.
+__global__ void head_flags_kernel(const int* __restrict__ crp, int mne, unsigned* __restrict__ f) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r <= mne;
+       r += (long long)gridDim.x * blockDim.x) {
+    const unsigned p = (unsigned)crp[r];
+    atomicOr(f + (p >> 5), 1u << (p & 31));
+  }
+}
+
 // Tile plan: rlo[t] = lower_bound(crp, t*TS) for t < ntiles, rlo[ntiles] = mne.
 __global__ void tile_plan_kernel(const int* __restrict__ crp, int mne, long long ntiles,
                                  long long TS, int* __restrict__ rlo) {

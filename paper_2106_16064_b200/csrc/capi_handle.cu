@@ -45,6 +45,8 @@ const Knob kKnobs[] = {
     {"hub_two_pass", "SPMK_HUB_TWO_PASS", &Tuning::hub_two_pass},
     {"hub_smem", "SPMK_HUB_SMEM", &Tuning::hub_smem},
     {"l2_persist", "SPMK_L2_PERSIST", &Tuning::l2_persist},
+    {"parws_impl", "SPMK_PARWS_IMPL", &Tuning::parws_impl},
+    {"parws_cpt", "SPMK_PARWS_CPT", &Tuning::parws_cpt},
 };
 }  // namespace
 
@@ -98,6 +100,7 @@ void free_handle(spmk_csr_s* h) {
   if (h->own_rp) cudaFree(h->rp);
   if (h->own_col) cudaFree(h->col);
   if (h->own_val) cudaFree(h->val);
+  cudaFree(h->hflag32);
   cudaFree(h->crp);
   cudaFree(h->rid);
   cudaFree(h->erow);
@@ -168,6 +171,18 @@ void build_meta(spmk_csr_s* h, cudaStream_t s) {
 }  // namespace
 
 // Plan for a nonzero-split kernel: tiles of TS nonzeros made of CH-chunks.
+// Segment-head flags of the 32-nonzero chunks (par_ws2.cuh), once per handle.
+const unsigned* get_head_flags32(spmk_csr_s* h, cudaStream_t s) {
+  if (h->hflag32) return h->hflag32;
+  const long long words = (h->nnz + 31) / 32 + 1;
+  unsigned* f = dev_alloc<unsigned>((size_t)words);
+  CK(cudaMemsetAsync(f, 0, (size_t)words * 4, s));
+  head_flags_kernel<<<grid_for((long long)h->mne + 1), 256, 0, s>>>(h->crp, h->mne, f); LAUNCHED(1);
+  CK(cudaGetLastError());
+  h->hflag32 = f;
+  return f;
+}
+
 Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EXT, cudaStream_t s) {
   EXT = std::max(1LL, std::min(EXT, TS));
   auto key = std::make_tuple(kind, TS, CH, EXT);

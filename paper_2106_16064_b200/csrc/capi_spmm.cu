@@ -229,10 +229,19 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws64(a, slots, s);
       timing_record(2, s);
     } else {
-      // T chunks of W nonzeros per tile (4 or 8: the two compiled shapes)
+      // W = 32, N <= 4 (the rule's par-ws regime): the streaming head-flag
+      // kernel, tiles of C chunks sized for ~48 resident warps per SM;
+      // otherwise T chunks of W nonzeros per tile (4 or 8: the two compiled shapes)
+      const bool ws2 = W == 32 && N <= 4 && h->tune.parws_impl == 2;
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
-      const long long TS = CH * T;
+      long long cpt = h->tune.parws_cpt;
+      if (ws2 && cpt <= 0) {
+        const long long chunks = (h->nnz + 31) / 32;
+        cpt = 4;
+        while (cpt < 64 && chunks / (cpt * 2) >= 148LL * 48) cpt *= 2;
+      }
+      const long long TS = ws2 ? CH * cpt : CH * T;
       Plan& p = get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
       a.rlo = p.rlo;
       a.desc = p.desc;
@@ -244,8 +253,10 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         a.H = sc;
         a.Tsl = sc + (size_t)nch * N;
       }
+      const unsigned* hf = ws2 ? get_head_flags32(h, s) : nullptr;
       timing_record(1, s);
-      launch_par_ws(a, W, T, aligned, s);
+      if (ws2) launch_par_ws2(a, hf, aligned, s);
+      else launch_par_ws(a, W, T, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0) launch_fixup(p, a.H, a.Tsl, d_y, N, s);
     }

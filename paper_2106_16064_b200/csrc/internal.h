@@ -117,6 +117,8 @@ struct Tuning {
   long long hub_two_pass = -1;   // -1 automatic (par-rs on, seq-rs off)
   long long hub_smem = 0;        // shared-memory pad of the seq-rs hub CTA
   long long l2_persist = 0;      // 1 = access-policy window over X on every spmm
+  long long parws_impl = 2;      // par-ws at lane_width 32, N <= 4: 2 = streaming head-flag kernel (par_ws2.cuh), 1 = tile kernel
+  long long parws_cpt = 0;       // par_ws2 chunks per tile (0 = automatic)
   void from_env();
   bool set(const std::string& key, long long v);
   bool get(const std::string& key, long long* v) const;
@@ -148,6 +150,7 @@ struct spmk_csr_s {
   int* rid = nullptr;     // mne
   int nempty = 0;
   int* erow = nullptr;    // nempty
+  unsigned* hflag32 = nullptr;  // segment heads of the 32-nonzero chunks (par_ws2), lazily built
   long long max_row = 0;
   unsigned long long sum_len2 = 0;
   spmk_host::Tuning tune;
@@ -183,6 +186,7 @@ spmk_status create_from_device32(long long m, long long k, long long nnz, int* r
                                  bool own, int device, spmk_csr_t* out, cudaStream_t s);
 Plan& get_plan(spmk_csr_s* h, int kind, long long TS, long long CH, long long EXT, cudaStream_t s);
 Plan& get_hub_plan(spmk_csr_s* h, int L, cudaStream_t s);
+const unsigned* get_head_flags32(spmk_csr_s* h, cudaStream_t s);
 Plan& get_rs_desc(spmk_csr_s* h, long long TS, int L, const Plan* hub, cudaStream_t s);
 void launch_zero_all(float* y, long long total, cudaStream_t s);
 void launch_zero_rows(const spmk_csr_s* h, int N, float* y, bool vec4, cudaStream_t s);
@@ -224,6 +228,7 @@ struct ParLaunch {
 void launch_par_rs(const ParLaunch& a, int W, int vl, bool aligned, cudaStream_t s);
 void launch_par_ws(const ParLaunch& a, int W, int T, bool aligned, cudaStream_t s);
 void launch_par_ws64(const ParLaunch& a, float* slots, cudaStream_t s);  // lane_width 64
+void launch_par_ws2(const ParLaunch& a, const unsigned* hflag, bool aligned, cudaStream_t s);  // W 32, N <= 4
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, int L, const float* d_x, int N,
                  float* d_y, cudaStream_t s);
 void launch_hub_rows(const int* crp, int mne, int L, int2* list, int* cnt, cudaStream_t s);

@@ -13,6 +13,7 @@
 #include "par_kernels.cuh"
 #include "par_ws.cuh"
 #include "par_ws64.cuh"
+#include "par_ws2.cuh"
 
 using namespace spmk_dev;
 
@@ -187,6 +188,21 @@ void launch_par_ws(const ParLaunch& l, int W, int T, bool aligned, cudaStream_t 
   const ParArgs a = to_args(l);
   if (T == 8) launch_par_ws_tt<8, 4>(a, W, aligned, s);
   else launch_par_ws_tt<4, 5>(a, W, aligned, s);
+}
+
+void launch_par_ws2(const ParLaunch& l, const unsigned* hflag, bool aligned, cudaStream_t s) {
+  ParWs2Args A{to_args(l), hflag};
+  const int N = A.p.N;
+  const int ct = N <= 1 ? 1 : N <= 2 ? 2 : 4;
+  A.p.xvec = aligned && ((ct == 4 && N % 4 == 0) || (ct == 2 && N % 2 == 0));
+  A.p.ncol_tile = ct;
+  const dim3 grid((unsigned)((A.p.nunits + 7) / 8), (unsigned)((N + ct - 1) / ct));
+  switch (ct) {
+    case 1: par_ws2_kernel<1, 4><<<grid, 256, 0, s>>>(A); break;
+    case 2: par_ws2_kernel<2, 4><<<grid, 256, 0, s>>>(A); break;
+    default: par_ws2_kernel<4, 4><<<grid, 256, 0, s>>>(A); break;
+  }
+  LAUNCHED(1);
 }
 
 void launch_par_ws64(const ParLaunch& l, float* slots, cudaStream_t s) {
