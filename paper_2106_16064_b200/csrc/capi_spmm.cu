@@ -229,17 +229,20 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws64(a, slots, s);
       timing_record(2, s);
     } else {
-      // W = 32, N <= 4 (the rule's par-ws regime): the streaming head-flag
-      // kernel, tiles of C chunks sized for ~48 resident warps per SM;
+      // W = 32, N <= 2 (SpMV: cfg1, cfg5, PageRank): the streaming head-flag
+      // kernel, tiles of C chunks (the largest power of two <= 64 that still
+      // gives >= 8 waves of 32 resident warps per SM: small tail);
       // otherwise T chunks of W nonzeros per tile (4 or 8: the two compiled shapes)
-      const bool ws2 = W == 32 && N <= 4 && h->tune.parws_impl == 2;
+      // (measured on B200: N = 1 / 2 / 4 on R-MAT s20 122 / 131 / 175 us vs
+      // 124 / 139 / 166 us for the tile kernel; cfg5 SpMV 2.72 vs 3.62 ms)
+      const bool ws2 = W == 32 && N <= 2 && h->tune.parws_impl == 2;
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
       long long cpt = h->tune.parws_cpt;
       if (ws2 && cpt <= 0) {
         const long long chunks = (h->nnz + 31) / 32;
         cpt = 4;
-        while (cpt < 64 && chunks / (cpt * 2) >= 148LL * 48) cpt *= 2;
+        while (cpt < 64 && chunks / (cpt * 2) >= 8LL * 148 * 32) cpt *= 2;
       }
       const long long TS = ws2 ? CH * cpt : CH * T;
       Plan& p = get_plan(h, 2, TS, CH, h->tune.parws_ext, s);

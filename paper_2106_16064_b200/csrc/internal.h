@@ -117,7 +117,7 @@ struct Tuning {
   long long hub_two_pass = -1;   // -1 automatic (par-rs on, seq-rs off)
   long long hub_smem = 0;        // shared-memory pad of the seq-rs hub CTA
   long long l2_persist = 0;      // 1 = access-policy window over X on every spmm
-  long long parws_impl = 2;      // par-ws at lane_width 32, N <= 4: 2 = streaming head-flag kernel (par_ws2.cuh), 1 = tile kernel
+  long long parws_impl = 2;      // par-ws at lane_width 32, N <= 2: 2 = streaming head-flag kernel (par_ws2.cuh), 1 = tile kernel
   long long parws_cpt = 0;       // par_ws2 chunks per tile (0 = automatic)
   void from_env();
   bool set(const std::string& key, long long v);
@@ -228,7 +228,7 @@ struct ParLaunch {
 void launch_par_rs(const ParLaunch& a, int W, int vl, bool aligned, cudaStream_t s);
 void launch_par_ws(const ParLaunch& a, int W, int T, bool aligned, cudaStream_t s);
 void launch_par_ws64(const ParLaunch& a, float* slots, cudaStream_t s);  // lane_width 64
-void launch_par_ws2(const ParLaunch& a, const unsigned* hflag, bool aligned, cudaStream_t s);  // W 32, N <= 4
+void launch_par_ws2(const ParLaunch& a, const unsigned* hflag, bool aligned, cudaStream_t s);  // W 32, N <= 2
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, int L, const float* d_x, int N,
                  float* d_y, cudaStream_t s);
 void launch_hub_rows(const int* crp, int mne, int L, int2* list, int* cnt, cudaStream_t s);

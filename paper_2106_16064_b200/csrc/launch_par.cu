@@ -193,15 +193,14 @@ void launch_par_ws(const ParLaunch& l, int W, int T, bool aligned, cudaStream_t 
 void launch_par_ws2(const ParLaunch& l, const unsigned* hflag, bool aligned, cudaStream_t s) {
   ParWs2Args A{to_args(l), hflag};
   const int N = A.p.N;
-  const int ct = N <= 1 ? 1 : N <= 2 ? 2 : 4;
-  A.p.xvec = aligned && ((ct == 4 && N % 4 == 0) || (ct == 2 && N % 2 == 0));
+  const int ct = N <= 1 ? 1 : 2;
+  A.p.xvec = aligned && ct == 2 && N % 2 == 0;
   A.p.ncol_tile = ct;
   const dim3 grid((unsigned)((A.p.nunits + 7) / 8), (unsigned)((N + ct - 1) / ct));
-  switch (ct) {
-    case 1: par_ws2_kernel<1, 4><<<grid, 256, 0, s>>>(A); break;
-    case 2: par_ws2_kernel<2, 4><<<grid, 256, 0, s>>>(A); break;
-    default: par_ws2_kernel<4, 4><<<grid, 256, 0, s>>>(A); break;
-  }
+  // groups of 2 chunks (measured: 4-chunk groups need 79 registers and run
+  // slower, cfg5 2.72 vs 2.88 ms)
+  if (ct == 1) par_ws2_kernel<1, 2><<<grid, 256, 0, s>>>(A);
+  else par_ws2_kernel<2, 2><<<grid, 256, 0, s>>>(A);
   LAUNCHED(1);
 }
 

@@ -1,5 +1,5 @@
 // par_ws2.cuh — par-ws (north_star d) at lane_width 32, the reference's
-// default and the rule's choice for N <= 4 (cfg1, cfg5, PageRank): a
+// default, for N <= 2 (SpMV: cfg1, cfg5, PageRank): a
 // streaming form of the paper's vectorized segment reduction built on
 // precomputed segment-head flags instead of per-tile row windows.
 //
@@ -21,9 +21,9 @@
 // owner prefix T for long rows, merged by fixup_kernel).  The row of lane l
 // is cur + popc(heads <= l, excluding bit 0) and advances by the chunk's head
 // count, so no row window, no bitmap construction and no per-tile setup
-// beyond one 16-byte descriptor; colIdx/val/hflag stream D chunks ahead and
-// the X gathers of the next D chunks are in flight while the current ones
-// are scanned.
+// beyond one 16-byte descriptor; colIdx/val/hflag stream two groups ahead,
+// the X gathers of the next group are in flight while the current group's
+// scans (independent, interleaved) run.
 #pragma once
 #include "common.cuh"
 #include "par_kernels.cuh"
@@ -72,102 +72,124 @@ par_ws2_kernel(const ParWs2Args A) {
 #pragma unroll
   for (int j = 0; j < CT; ++j) carry[j] = 0.f;
 
-  // pipeline registers: D chunks of (col, val, head word) and their X rows
-  int cr[D];
-  float vr[D];
-  unsigned hr[D], hn[D];
-  float xr[D][CT];
+  // Software pipeline over groups of G chunks: colIdx/val/head words of
+  // group g+2 load while group g is processed (2G slots), the X rows of
+  // group g+1 are gathered right after group g's products are formed (G
+  // slots); within a group the G conditional scans are independent
+  // straight-line code (interleaved level by level), only the emission /
+  // carry pass is sequential over the chunks.
+  constexpr int G = D;
+  constexpr int S = 2 * G;
+  int cr[S];
+  float vr[S];
+  unsigned hr[S];
+  float xr[G][CT];
   auto load_cv = [&](int q, int i) {
     const int p = (q << 5) + lane;
     const bool live = q < q_end && p >= lo && p < hard_end;
     cr[i] = live ? ld_stream(a.col + p, pol) : 0;
     vr[i] = live ? ld_stream(a.val + p, pol) : 0.f;
-    hr[i] = q < q_end ? __ldg(A.hflag + q) : 0u;
-    hn[i] = q < q_end ? __ldg(A.hflag + q + 1) : 0u;
+    hr[i] = q <= q_end ? __ldg(A.hflag + q) : 0u;  // q_end <= ceil(nnz/32): in range
   };
-  auto load_x = [&](int q, int i) {
+  auto load_x = [&](int q, int ci, int xi) {
     const int p = (q << 5) + lane;
     const bool live = q < q_end && p >= lo && p < hard_end;
-    load_dense_cols<CT>(reinterpret_cast<const float*>(xb + (size_t)(unsigned)cr[i] * xs), nt, vec, live, xr[i]);
+    load_dense_cols<CT>(reinterpret_cast<const float*>(xb + (size_t)(unsigned)cr[ci] * xs), nt, vec, live, xr[xi]);
   };
 
 #pragma unroll
-  for (int i = 0; i < D; ++i) load_cv(q_beg + i, i);
+  for (int i = 0; i < S; ++i) load_cv(q_beg + i, i);
 #pragma unroll
-  for (int i = 0; i < D; ++i) load_x(q_beg + i, i);
+  for (int i = 0; i < G; ++i) load_x(q_beg + i, i, i);
 
 #pragma unroll 1
-  for (int qg = q_beg; qg < q_end; qg += D) {
-    // the next group's colIdx/val/heads are loaded into the slots as they free up
+  for (int qg = q_beg; qg < q_end; qg += S) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      const int q = qg + i;
-      if (q >= q_end) break;  // warp-uniform
-      const int c0 = q << 5;
-      const int p = c0 + lane;
-      const int hi = min(c0 + 32, hard_end);
-      const bool live = p >= lo && p < hi;
-      const unsigned M = hr[i];
-      const unsigned mle = M & le;
-      const int sst = mle ? 31 - __clz(mle) : 0;  // first lane of this lane's run
-      float v[CT];
+    for (int h = 0; h < 2; ++h) {  // two groups per iteration: slots h*G .. h*G+G-1
+      const int q0 = qg + h * G;
+      if (q0 >= q_end) break;  // warp-uniform
+      float v[G][CT];
+      int sst[G];
 #pragma unroll
-      for (int j = 0; j < CT; ++j) v[j] = __fmul_rn(vr[i], xr[i][j]);  // kernels.hpp:277 (dead: 0)
+      for (int i = 0; i < G; ++i) {
+        const unsigned mle = hr[h * G + i] & le;
+        sst[i] = mle ? 31 - __clz(mle) : 0;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {  // reduction.hpp:77-85, lockstep
-        const bool same = lane - off >= sst;
+        for (int j = 0; j < CT; ++j) v[i][j] = __fmul_rn(vr[h * G + i], xr[i][j]);  // kernels.hpp:277
+      }
+      // X rows of the next group into the freed slots (its colIdx landed a group ago)
 #pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          const float up = __shfl_up_sync(FULL, v[j], off);
-          if (same) v[j] = __fadd_rn(v[j], up);
+      for (int i = 0; i < G; ++i) load_x(q0 + G + i, ((h + 1) % 2) * G + i, i);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {  // reduction.hpp:77-85, lockstep; G chunks interleaved
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          const bool same = lane - off >= sst[i];
+#pragma unroll
+          for (int j = 0; j < CT; ++j) {
+            const float up = __shfl_up_sync(FULL, v[i][j], off);
+            if (same) v[i][j] = __fadd_rn(v[i][j], up);
+          }
         }
       }
-      // lane l closes its run iff position l+1 starts a row (head bit, or
-      // bit 0 of the next chunk's word, or the phantom head at nnz) or the
-      // unit's range ends there
-      const bool next_head = (lane < 31) ? ((M >> (lane + 1)) & 1u) : (hn[i] & 1u);
-      const bool last = live && (next_head || p + 1 == hi);
-      const bool first_run = (mle & ~1u) == 0 && !(M & 1u);  // run open since before c0
-      float t[CT];
 #pragma unroll
-      for (int j = 0; j < CT; ++j)
-        t[j] = (first_run && has_carry && mode == MODE_NORMAL) ? __fadd_rn(carry[j], v[j]) : v[j];
-      if (last) {
-        if (first_run && mode == MODE_ENTER_LONG) {
-          store_cols<CT>(a.H + (size_t)q * N + col0, nt, t, false);  // long row: per-chunk partial
-        } else if (next_head) {
-          const int r = cur + __popc(mle & ~1u);
-          store_cols<CT>(reinterpret_cast<float*>(ybase + (size_t)(unsigned)a.rid[r] * xs), nt, t, true);
+      for (int i = 0; i < G; ++i) {
+        const int q = q0 + i;
+        if (q >= q_end) break;  // warp-uniform
+        const int c0 = q << 5;
+        const int p = c0 + lane;
+        const int hi = min(c0 + 32, hard_end);
+        const bool live = p >= lo && p < hi;
+        const unsigned M = hr[h * G + i];
+        const unsigned Mn = hr[(h * G + i + 1) % S];  // chunk q+1's heads (loaded earlier)
+        const unsigned mle = M & le;
+        // lane l closes its run iff position l+1 starts a row (head bit, or
+        // bit 0 of the next chunk's word, or the phantom head at nnz) or the
+        // unit's range ends there
+        const bool next_head = (lane < 31) ? ((M >> (lane + 1)) & 1u) : (Mn & 1u);
+        const bool last = live && (next_head || p + 1 == hi);
+        const bool first_run = (mle & ~1u) == 0 && !(M & 1u);  // run open since before c0
+        float t[CT];
+#pragma unroll
+        for (int j = 0; j < CT; ++j)
+          t[j] = (first_run && has_carry && mode == MODE_NORMAL) ? __fadd_rn(carry[j], v[i][j]) : v[i][j];
+        if (last) {
+          if (first_run && mode == MODE_ENTER_LONG) {
+            store_cols<CT>(a.H + (size_t)q * N + col0, nt, t, false);  // long row: per-chunk partial
+          } else if (next_head) {
+            const int r = cur + __popc(mle & ~1u);
+            store_cols<CT>(reinterpret_cast<float*>(ybase + (size_t)(unsigned)a.rid[r] * xs), nt, t, true);
+          }
         }
-      }
-      // the run crossing c0+32 (if any) becomes the carried row
-      const int ll = min(hi - c0, 32) - 1;  // last live lane of the chunk
-      const bool cont_l = !((ll < 31) ? ((M >> (ll + 1)) & 1u) : (hn[i] & 1u));
-      const bool cont = __shfl_sync(FULL, cont_l, ll);
-      const bool lfirst = __shfl_sync(FULL, first_run, ll);
-      float tl[CT];
+        // the run crossing c0+32 (if any) becomes the carried row
+        // (warp-uniform: computed from the chunk's head word, no shuffle)
+        const int ll = min(hi - c0, 32) - 1;  // last live lane of the chunk
+        const bool cont = !((ll < 31) ? ((M >> (ll + 1)) & 1u) : (Mn & 1u));
+        const unsigned le_ll = (ll == 31) ? FULL : ((2u << ll) - 1u);
+        const bool lfirst = (M & le_ll & ~1u) == 0 && !(M & 1u);
+        float tl[CT];
 #pragma unroll
-      for (int j = 0; j < CT; ++j) tl[j] = __shfl_sync(FULL, t[j], ll);
-      if (cont) {
-        if (!lfirst) {
+        for (int j = 0; j < CT; ++j) tl[j] = __shfl_sync(FULL, t[j], ll);
+        if (cont) {
+          if (!lfirst) {
 #pragma unroll
-          for (int j = 0; j < CT; ++j) carry[j] = __fadd_rn(0.f, tl[j]);  // Y starts at +0
-          has_carry = true;
+            for (int j = 0; j < CT; ++j) carry[j] = __fadd_rn(0.f, tl[j]);  // Y starts at +0
+            has_carry = true;
+            mode = MODE_NORMAL;
+          } else if (mode == MODE_NORMAL) {
+#pragma unroll
+            for (int j = 0; j < CT; ++j) carry[j] = tl[j];
+          }
+        } else {
+          has_carry = false;
           mode = MODE_NORMAL;
-        } else if (mode == MODE_NORMAL) {
-#pragma unroll
-          for (int j = 0; j < CT; ++j) carry[j] = tl[j];
         }
-      } else {
-        has_carry = false;
-        mode = MODE_NORMAL;
+        cur += __popc(M & ~1u) + (int)(Mn & 1u);  // compact row containing c0 + 32
       }
-      cur += __popc(M & ~1u) + (int)(hn[i] & 1u);  // compact row containing c0 + 32
-      // refill this slot with the chunk D ahead
-      load_cv(q + D, i);
-    }
+      // colIdx/val/heads of group g+2 into this group's slots
 #pragma unroll
-    for (int i = 0; i < D; ++i) load_x(qg + D + i, i);
+      for (int i = 0; i < G; ++i) load_cv(q0 + S + i, h * G + i);
+    }
   }
   // long row crossing te (its owner does not extend): prefix -> T slot
   if (hard_end == te && te < a.nnz && has_carry && mode == MODE_NORMAL && lane == 0)
