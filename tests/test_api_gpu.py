@@ -75,3 +75,35 @@ def test_error_paths(mat):
                  cfg=spmk.KernelConfig(lane_width=128))
     with pytest.raises(spmk.Error):
         spmk.DeviceCsr.generate_rmat(0, 8)
+
+
+def test_l2_access_policy_window_keeps_bits(mat):
+    """The X access-policy window (tuning knob l2_persist, spmk_l2_persist_x)
+    changes cache residency only: every variant gives the same bits with and
+    without it.  (Measured on B200 it is slower for cfg2 / cfg4 — 271 -> 306 us,
+    12.8 -> 14.1 ms — so it stays off by default.)"""
+    x = torch.randn(mat.num_cols, 32, device="cuda")
+    ref = {k.name: mat.spmm(k, x).clone() for k in spmk.kAllKernels}
+    mat.set_tuning("l2_persist", 1)
+    try:
+        for k in spmk.kAllKernels:
+            assert torch.equal(mat.spmm(k, x), ref[k.name]), k.name
+    finally:
+        mat.set_tuning("l2_persist", 0)
+        spmk.l2_persist_x(torch.cuda.current_stream(), None)
+
+
+def test_tuning_knobs_keep_bits(mat):
+    """Every performance knob picks tile shapes / kernel paths, never a
+    summation order: par-ws through the tile kernel (parws_impl=1) and the
+    streaming kernel (2) at several tile sizes give identical bits."""
+    x = torch.randn(mat.num_cols, 2, device="cuda")
+    ref = mat.spmm(spmk.kParBalanced, x).clone()
+    try:
+        for impl, cpt in ((1, 0), (2, 4), (2, 16), (2, 64)):
+            mat.set_tuning("parws_impl", impl)
+            mat.set_tuning("parws_cpt", cpt)
+            assert torch.equal(mat.spmm(spmk.kParBalanced, x), ref), (impl, cpt)
+    finally:
+        mat.set_tuning("parws_impl", 2)
+        mat.set_tuning("parws_cpt", 0)
