@@ -47,6 +47,8 @@ const Knob kKnobs[] = {
     {"l2_persist", "SPMK_L2_PERSIST", &Tuning::l2_persist},
     {"parws_impl", "SPMK_PARWS_IMPL", &Tuning::parws_impl},
     {"parws_cpt", "SPMK_PARWS_CPT", &Tuning::parws_cpt},
+    {"seq_impl", "SPMK_SEQ_IMPL", &Tuning::seq_impl},
+    {"sell_cfg", "SPMK_SELL_CFG", &Tuning::sell_cfg},
 };
 }  // namespace
 
@@ -110,6 +112,7 @@ void free_handle(spmk_csr_s* h) {
     cudaFree(kv.second.longrows);
     cudaFree(kv.second.longinfo);
   }
+  for (auto& kv : h->sell_plans) free_sell_plan(kv.second);
   h->scratch.release();
   for (auto& kv : h->hub_layouts) {
     cudaFree(kv.second.po);

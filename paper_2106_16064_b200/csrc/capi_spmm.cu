@@ -147,11 +147,14 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // overlap the gather-bound sweep; capturable into CUDA graphs).
   // Row-split variants: hub rows (>= L nonzeros) run in hub_kernels.cuh on
   // the side stream, concurrently with the main kernel (disjoint rows of Y).
+  // seq-ws at N % 32 == 0: the lane-per-job sweep writes the empty rows itself
+  const bool sell = id == SPMK_SEQ_BALANCED && sell_eligible(h, (long long)cfg.seq_chunk, N, aligned);
   const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
   const int L = rs ? hub_threshold(h, id) : 0;
   const Plan* hub = L > 0 ? &get_hub_plan(h, L, s) : nullptr;
   const bool hubs = hub && hub->nlong > 0;
-  const bool fork = h->nempty > 0 || hubs;
+  const bool zero_side = h->nempty > 0 && !sell;
+  const bool fork = zero_side || hubs;
   if (fork) {
     if (!h->side) {
       CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -161,7 +164,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     CK(cudaEventRecord(h->ev_fork, s));
     CK(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
     if (hubs) launch_hubs(h, *hub, id, (int)cfg.lane_width, L, d_x, N, d_y, h->side);
-    if (h->nempty > 0) launch_zero_rows(h, N, d_y, aligned && N % 4 == 0, h->side);
+    if (zero_side) launch_zero_rows(h, N, d_y, aligned && N % 4 == 0, h->side);
     CK(cudaEventRecord(h->ev_join, h->side));
   }
 
@@ -183,6 +186,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       a.desc = p.desc;
       timing_record(1, s);
       launch_seq(a, false, aligned, s);
+      timing_record(2, s);
+    } else if (sell) {
+      SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, s);
+      float* H = sp.nslots > 0 ? h->scratch.get((size_t)sp.nslots * N) : nullptr;
+      timing_record(1, s);
+      launch_sell(h, sp, d_x, N, d_y, H, s);
       timing_record(2, s);
     } else {
       const long long CH = (long long)cfg.seq_chunk;

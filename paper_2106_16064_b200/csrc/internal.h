@@ -95,6 +95,21 @@ struct Plan {
   std::vector<int> hlen;     // hub plans: hub row lengths in launch order
 };
 
+// Lane-per-job seq-ws layout (sell_kernels.cuh), per seq_chunk.
+constexpr long long kSellMaxChunk = 512;
+struct SellPlan {
+  long long CH = 0;
+  int shape = 0;            // sweep shape (launch_sell.cu kSellShapes)
+  int* steps = nullptr;     // nsteps x 64 ints
+  long long nsteps = 0;
+  int* wstep = nullptr;     // nwarps + 1 range starts
+  int nwarps = 0, blocks = 0;
+  int4* fold = nullptr;     // {row, first slot, slots} of the rows of >= 3 segments
+  int nfold = 0;
+  int nbig = 0;             // leading fold rows with > kFoldWarpMax slots (one CTA each)
+  long long nslots = 0;     // H slots (x N floats)
+};
+
 // Products-buffer layout of the hub rows for one N (par-rs two-pass path).
 struct HubLayout {
   long long* po = nullptr;  // per hub: offset in floats (multiple of 4)
@@ -119,6 +134,8 @@ struct Tuning {
   long long l2_persist = 0;      // 1 = access-policy window over X on every spmm
   long long parws_impl = 2;      // par-ws at lane_width 32, N <= 2: 2 = streaming head-flag kernel (par_ws2.cuh), 1 = tile kernel
   long long parws_cpt = 0;       // par_ws2 chunks per tile (0 = automatic)
+  long long sell_cfg = 0;        // lane-per-job sweep shape (launch_sell.cu)
+  long long seq_impl = 2;        // seq-ws, seq_chunk <= kSellMaxChunk: 2 = lane-per-job sweep (sell_kernels.cuh) at N = 32, 3 = also at N % 32 == 0, 1 = tile sweep only
   void from_env();
   bool set(const std::string& key, long long v);
   bool get(const std::string& key, long long* v) const;
@@ -157,6 +174,7 @@ struct spmk_csr_s {
   // caches
   std::map<std::tuple<int, long long, long long, long long>, spmk_host::Plan> plans;
   spmk_host::GrowBuffer scratch;   // long-row partial slots (H, T)
+  std::map<std::pair<long long, int>, spmk_host::SellPlan> sell_plans;  // (seq_chunk, shape)
   std::map<std::pair<int, int>, spmk_host::HubLayout> hub_layouts;  // (L, N)
   spmk_host::GrowBuffer hub_prod;  // par-rs two-pass hub products
   // host-operand staging: kStageSlots rotating (X, Y) device buffer pairs;
@@ -209,6 +227,12 @@ struct SeqLaunch {
   long long TS, CH, EXT;
 };
 void launch_seq(const SeqLaunch& a, bool ws, bool aligned, cudaStream_t s);
+
+// ---- launch_sell.cu
+bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned);
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s);
+void free_sell_plan(SellPlan& p);
+void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s);
 
 // ---- launch_par.cu
 struct ParLaunch {

@@ -1,0 +1,233 @@
+// launch_sell.cu — plan and launch of the lane-per-job seq-ws sweep
+// (sell_kernels.cuh; spmm_seq_balanced kernels.hpp:384-455).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+#include "sell_kernels.cuh"
+
+using namespace spmk_dev;
+
+namespace spmk_host {
+namespace {
+
+// Sweep shapes (ring depths S / C, warps per CTA, CTAs per SM); tuning knob
+// sell_cfg picks one (measured on B200).
+struct SellShape {
+  const void* fn;
+  void (*launch)(dim3, const SellArgs&, cudaStream_t);
+  int wpc, smem;
+};
+template <int S, int C, int WPC, int MINB>
+void sell_launch_t(dim3 grid, const SellArgs& a, cudaStream_t s) {
+  seq_sell_kernel<S, C, WPC, MINB><<<grid, WPC * 32, sell_smem_bytes<S, C, WPC>(), s>>>(a);
+}
+template <int S, int C, int WPC, int MINB>
+constexpr SellShape sell_shape() {
+  return SellShape{reinterpret_cast<const void*>(seq_sell_kernel<S, C, WPC, MINB>), sell_launch_t<S, C, WPC, MINB>,
+                   WPC, sell_smem_bytes<S, C, WPC>()};
+}
+const SellShape kSellShapes[] = {
+    sell_shape<4, 8, 4, 3>(),   // 0: 12 warps / SM, 3 steps of rows in flight per warp
+    sell_shape<2, 8, 8, 2>(),   // 1: 16 warps, 1 in flight
+    sell_shape<4, 8, 12, 1>(),  // 2: 12 warps in one CTA
+    sell_shape<8, 16, 3, 2>(),  // 3: 6 warps, 7 in flight
+};
+constexpr int kSellShapeCount = sizeof(kSellShapes) / sizeof(kSellShapes[0]);
+
+template <typename T>
+struct DevTmp {
+  T* p = nullptr;
+  explicit DevTmp(size_t n) { p = dev_alloc<T>(n); }
+  ~DevTmp() { cudaFree(p); }
+  DevTmp(const DevTmp&) = delete;
+  DevTmp& operator=(const DevTmp&) = delete;
+};
+
+template <typename In, typename Out>
+void exclusive_scan(const In* in, Out* out, int n, cudaStream_t s) {
+  size_t bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+  DevTmp<unsigned char> tmp(bytes);
+  CK(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
+}
+
+__global__ void fold_keys_kernel(const int4* f, int n, int* key, int* idx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    key[i] = f[i].z;
+    idx[i] = i;
+  }
+}
+__global__ void gather_int4_kernel(const int4* in, const int* idx, int n, int4* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = in[idx[i]];
+}
+__global__ void iota_kernel(int* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+// Resident CTAs per SM of a sweep shape (and its shared-memory opt-in), per device.
+int sell_blocks_per_sm(int shape) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, shape});
+  if (it != cache.end()) return it->second;
+  const SellShape& sh = kSellShapes[shape];
+  int bps = 1;
+  CK(cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sh.fn, sh.wpc * 32, sh.smem));
+  if (bps < 1) bps = 1;
+  cache[{dev, shape}] = bps;
+  return bps;
+}
+
+int sell_shape_of(const spmk_csr_s* h) {
+  const long long v = h->tune.sell_cfg;
+  return v >= 0 && v < kSellShapeCount ? (int)v : 0;
+}
+
+}  // namespace
+
+bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned) {
+  // N = 32 only: at N = 64 / 128 the tile sweep (16 / 32 lanes per unit,
+  // 256 / 512-byte rows per gather) measured 7 % / 34 % faster on B200
+  const bool shape_ok = h->tune.seq_impl == 2 ? N == 32 : (h->tune.seq_impl == 3 && N % 32 == 0);
+  return shape_ok && aligned && CH <= kSellMaxChunk && h->k < INT32_MAX &&
+         (unsigned long long)h->k * (unsigned long long)(N / 4) < (1ull << 32) &&
+         h->nnz < INT32_MAX && h->m < INT32_MAX;
+}
+
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
+  const int shape = sell_shape_of(h);
+  auto it = h->sell_plans.find({CH, shape});
+  if (it != h->sell_plans.end()) return it->second;
+  const int mne = h->mne;
+  SellPlan p;
+  p.CH = CH;
+  p.shape = shape;
+  // jobs per compact row, H slots, fold rows
+  DevTmp<int> njob(mne + 1), nslot(mne + 1), nmulti(mne + 1);
+  DevTmp<int> joff(mne + 1), soff(mne + 1), moff(mne + 1);
+  CK(cudaMemsetAsync(njob.p + mne, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(nslot.p + mne, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(nmulti.p + mne, 0, sizeof(int), s));
+  sell_count_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, mne, CH, njob.p, nslot.p, nmulti.p); LAUNCHED(1);
+  exclusive_scan(njob.p, joff.p, mne + 1, s);
+  exclusive_scan(nslot.p, soff.p, mne + 1, s);
+  exclusive_scan(nmulti.p, moff.p, mne + 1, s);
+  int tot[3];
+  CK(cudaMemcpyAsync(&tot[0], joff.p + mne, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&tot[1], soff.p + mne, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&tot[2], moff.p + mne, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int Jr = tot[0];
+  const int J = Jr + h->nempty;
+  p.nslots = tot[1];
+  p.nfold = tot[2];
+  DevTmp<int> jstart(J), jlen(J), jout(J);
+  if (p.nfold > 0) p.fold = dev_alloc<int4>(p.nfold);
+  sell_jobs_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, h->rid, mne, CH, joff.p, soff.p, moff.p, jstart.p,
+                                                 jlen.p, jout.p, p.fold); LAUNCHED(1);
+  if (p.nfold > 1) {  // fold rows with the most slots first (the jobs address H slots, not fold rows)
+    DevTmp<int> key(p.nfold), key_s(p.nfold), fidx(p.nfold), fidx_s(p.nfold);
+    DevTmp<int4> tmpf(p.nfold);
+    fold_keys_kernel<<<grid_for(p.nfold), 256, 0, s>>>(p.fold, p.nfold, key.p, fidx.p); LAUNCHED(1);
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, key.p, key_s.p, fidx.p, fidx_s.p, p.nfold, 0, 32, s));
+    DevTmp<unsigned char> tmp(bytes);
+    CK(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, key.p, key_s.p, fidx.p, fidx_s.p, p.nfold, 0, 32, s));
+    gather_int4_kernel<<<grid_for(p.nfold), 256, 0, s>>>(p.fold, fidx_s.p, p.nfold, tmpf.p); LAUNCHED(1);
+    CK(cudaMemcpyAsync(p.fold, tmpf.p, sizeof(int4) * p.nfold, cudaMemcpyDeviceToDevice, s));
+    std::vector<int> ks((size_t)p.nfold);
+    CK(cudaMemcpyAsync(ks.data(), key_s.p, sizeof(int) * p.nfold, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    while (p.nbig < p.nfold && ks[(size_t)p.nbig] > kFoldWarpMax) ++p.nbig;
+  } else if (p.nfold == 1) {
+    int4 f1;
+    CK(cudaMemcpyAsync(&f1, p.fold, sizeof(int4), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    p.nbig = f1.z > kFoldWarpMax ? 1 : 0;
+  }
+  if (h->nempty > 0) {
+    sell_empty_jobs_kernel<<<grid_for(h->nempty), 256, 0, s>>>(h->erow, h->nempty, Jr, jstart.p, jlen.p, jout.p); LAUNCHED(1);
+  }
+  // jobs by length, descending (stable: equal lengths keep row order)
+  DevTmp<int> idx(J), sidx(J), slen(J);
+  iota_kernel<<<grid_for(J), 256, 0, s>>>(idx.p, J); LAUNCHED(1);
+  {
+    size_t bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, jlen.p, slen.p, idx.p, sidx.p, J, 0, 16, s));
+    DevTmp<unsigned char> tmp(bytes);
+    CK(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, jlen.p, slen.p, idx.p, sidx.p, J, 0, 16, s));
+  }
+  const int nsl = (J + 31) / 32;
+  DevTmp<long long> lsteps(nsl + 1), lcost(nsl + 1), step_ex(nsl + 1), cost_ex(nsl + 1);
+  CK(cudaMemsetAsync(lsteps.p + nsl, 0, sizeof(long long), s));
+  CK(cudaMemsetAsync(lcost.p + nsl, 0, sizeof(long long), s));
+  sell_slice_kernel<<<grid_for(nsl), 256, 0, s>>>(slen.p, nsl, lsteps.p, lcost.p); LAUNCHED(1);
+  exclusive_scan(lsteps.p, step_ex.p, nsl + 1, s);
+  exclusive_scan(lcost.p, cost_ex.p, nsl + 1, s);
+  long long T = 0;
+  CK(cudaMemcpyAsync(&T, step_ex.p + nsl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (T >= INT32_MAX) throw CudaError{SPMK_EUNSUPPORTED, "sell layout: too many steps"};
+  p.nsteps = T;
+  p.steps = dev_alloc<int>((size_t)T * kSellStepInts);
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  p.blocks = sms * sell_blocks_per_sm(shape);
+  p.nwarps = p.blocks * kSellShapes[shape].wpc;
+  p.wstep = dev_alloc<int>((size_t)p.nwarps + 1);
+  sell_ranges_kernel<<<grid_for(p.nwarps + 1), 256, 0, s>>>(cost_ex.p, step_ex.p, nsl, p.nwarps, p.wstep); LAUNCHED(1);
+  sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, step_ex.p, jstart.p, jout.p,
+                                                                 h->col, h->val, p.steps); LAUNCHED(1);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));  // temporaries are freed on return
+  return h->sell_plans.emplace(std::make_pair(CH, shape), p).first->second;
+}
+
+void free_sell_plan(SellPlan& p) {
+  cudaFree(p.steps);
+  cudaFree(p.wstep);
+  cudaFree(p.fold);
+  p = SellPlan{};
+}
+
+void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s) {
+  const int tiles = N / 32;
+  SellArgs a{};
+  a.steps = p.steps;
+  a.wstep = p.wstep;
+  a.X = X;
+  a.Y = Y;
+  a.H = H;
+  a.N = N;
+  a.nwarps = p.nwarps;
+  a.one2 = kOnePair;
+  sell_blocks_per_sm(p.shape);  // shared-memory opt-in on this device
+  kSellShapes[p.shape].launch(dim3(p.blocks, tiles), a, s); LAUNCHED(1);
+  if (p.nfold > 0) {
+    // programmatic dependent launch: scheduled while the sweep drains
+    cudaLaunchConfig_t lc = {};
+    const long long small_warps = ((long long)(p.nfold - p.nbig) * tiles + kFoldRows - 1) / kFoldRows;
+    lc.gridDim = dim3((unsigned)((long long)p.nbig * tiles + (small_warps + 7) / 8));
+    lc.blockDim = dim3(256);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&lc, sell_fold_kernel, (const int4*)p.fold, p.nfold, p.nbig, (const float*)H, Y, N)); LAUNCHED(1);
+  }
+}
+
+}  // namespace spmk_host

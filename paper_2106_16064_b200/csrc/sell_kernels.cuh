@@ -1,0 +1,404 @@
+// sell_kernels.cuh — seq-ws (spmm_seq_balanced, kernels.hpp:384-455) as a
+// lane-per-job sweep over a segment-sliced layout of A.
+//
+// Decomposition (exact in the reference's order).  Cut every non-empty row at
+// the seq_chunk boundaries (multiples of CH): a piece of a row inside one chunk
+// is a *segment*.  The reference computes every segment as one sequential
+// chain acc = ((0 + v0 x0) + v1 x1) + ... (kernels.hpp:426-443), writes it
+// straight into Y when the row is complete in the chunk, into a boundary slot
+// otherwise, and folds the slots into the zero-initialised Y in ascending
+// chunk order: Y[r] = ((0 + P_first) + P_next) + ... (:448-453).  A *job* is
+//   * a row of one segment: one lane runs it and writes acc into Y (acc is
+//     never -0, so the reference's Y = acc and 0 + acc have the same bits);
+//   * one segment of a row that crosses a chunk boundary: its chain goes to
+//     an H slot (slots of a row are consecutive) and sell_fold_kernel folds
+//     the row's slots in ascending order after the sweep.  (Running rows of
+//     two segments in one lane with a carry measured 5 % slower: 32 more
+//     registers and a per-step boundary test, for a smaller fold);
+//   * an empty row (length 0): writes the zeros of Y.
+// Any assignment of jobs to lanes gives the same bits, so jobs are sorted by
+// length (descending, stable) and cut into slices of 32 (SELL-32): the lanes of
+// a warp run jobs of nearly equal length in lockstep (R-MAT s20: 0.5 % of the
+// data positions are padding).
+//
+// Layout in HBM (built once per handle and seq_chunk, sell_*_kernel below):
+// one *step* = 64 ints = 256 bytes = the 32 lanes' (column, value) at one
+// position.  A slice is a header step followed by L data steps:
+//   header: [lane] = output code (Y row, 0x80000000 | H slot, or -1 = none),
+//           [32 + lane] = the lane's job length (lane 0: the slice's L)
+//   data:   [lane] = column (0 for padding), [32 + lane] = value bits (0 for padding)
+// Padding positions (t >= the lane's job length) gather row 0 and are not added.
+//
+// Sweep (seq_sell_kernel): persistent warps, each over a contiguous range of
+// steps balanced at plan time.  Per warp, in shared memory, filled with
+// cp.async (LDGSTS, 16 B per lane, one commit group per iteration):
+//   * a C-stage ring of steps, C - 1 steps ahead of the consumer;
+//   * an S-stage ring of dense rows, S - 1 steps ahead: 8 LDGSTS per step,
+//     each copying 4 whole 128-B rows X[col, col0 .. col0 + 31] (lanes 8g..8g+7
+//     take rows 8g + i, one 16-B chunk each: every instruction coalesced).
+// Lane j reads its own row with 8 LDS.128 in rotated chunk order (chunk
+// (c + j) & 7 at step c: the 8 lanes of a quarter warp hit 8 different bank
+// groups; accumulator slot c holds columns 4((c + j) & 7) .. +3).  Measured:
+// an XOR-swizzled ring (chunk k of row r at k ^ (r & 7), static slots) was 24 %
+// slower on B200, a 144-byte padded row pitch cost 12.5 % of the ring's
+// in-flight bytes and was slower too.  The exact products / adds run as
+// FMUL2 / FFMA2-by-one pairs.  No shuffles and no per-nonzero row events (the
+// tile sweep of seq_kernels.cuh spends ~7.5 warp instructions per nonzero on
+// them).
+#pragma once
+#include "common.cuh"
+
+namespace spmk_dev {
+
+constexpr int kSellStepInts = 64;  // one step: 32 columns + 32 values
+
+// ---------------------------------------------------------------- plan
+// Per compact row: jobs (= segments), H slots and fold flag (rows of >= 2
+// segments).
+__global__ void sell_count_kernel(const int* __restrict__ crp, int mne, long long CH, int* __restrict__ njob,
+                                  int* __restrict__ nslot, int* __restrict__ nmulti) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mne; i += gridDim.x * blockDim.x) {
+    const long long s = crp[i], e = crp[i + 1];
+    const int nseg = (int)((e - 1) / CH - s / CH + 1);
+    const bool split = nseg > 1;
+    njob[i] = split ? nseg : 1;
+    nslot[i] = split ? nseg : 0;
+    nmulti[i] = split ? 1 : 0;
+  }
+}
+
+// Jobs of every compact row (offsets from exclusive scans of the counts) and
+// the fold list {row, first slot, slots, 0} of the split rows.
+__global__ void sell_jobs_kernel(const int* __restrict__ crp, const int* __restrict__ rid, int mne, long long CH,
+                                 const int* __restrict__ joff, const int* __restrict__ soff,
+                                 const int* __restrict__ moff, int* __restrict__ jstart, int* __restrict__ jlen,
+                                 int* __restrict__ jout, int4* __restrict__ fold) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mne; i += gridDim.x * blockDim.x) {
+    const long long s = crp[i], e = crp[i + 1];
+    const long long q0 = s / CH;
+    const long long nseg = (e - 1) / CH - q0 + 1;
+    const int j = joff[i];
+    if (nseg == 1) {
+      jstart[j] = (int)s;
+      jlen[j] = (int)(e - s);
+      jout[j] = rid[i];
+    } else {
+      const int s0 = soff[i];
+      for (long long k = 0; k < nseg; ++k) {
+        const long long a = k == 0 ? s : (q0 + k) * CH;
+        const long long b = k == nseg - 1 ? e : (q0 + k + 1) * CH;
+        jstart[j + k] = (int)a;
+        jlen[j + k] = (int)(b - a);
+        jout[j + k] = (int)(0x80000000u | (unsigned)(s0 + k));
+      }
+      fold[moff[i]] = make_int4(rid[i], s0, (int)nseg, 0);
+    }
+  }
+}
+
+// Empty rows: jobs of length 0 (their slice writes the zeros).
+__global__ void sell_empty_jobs_kernel(const int* __restrict__ erow, int nempty, int j0, int* __restrict__ jstart,
+                                       int* __restrict__ jlen, int* __restrict__ jout) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nempty; i += gridDim.x * blockDim.x) {
+    jstart[j0 + i] = 0;
+    jlen[j0 + i] = 0;
+    jout[j0 + i] = erow[i];
+  }
+}
+
+// Slice lengths (jobs sorted by length, descending: the slice's first job is
+// its longest) -> steps (1 + L) and balancing cost (steps + 1: the header and
+// the epilogue cost about one more step).
+__global__ void sell_slice_kernel(const int* __restrict__ slen_sorted, int nsl, long long* __restrict__ steps,
+                                  long long* __restrict__ cost) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x) {
+    const int L = slen_sorted[32 * s];
+    steps[s] = 1 + L;
+    cost[s] = 2 + L;
+  }
+}
+
+// First step of every warp's range: the first slice whose cost prefix reaches
+// w * total / W (contiguous ranges, cut at slice boundaries).
+__global__ void sell_ranges_kernel(const long long* __restrict__ cost_ex, const long long* __restrict__ step_ex,
+                                   int nsl, int W, int* __restrict__ wstep) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= W; w += gridDim.x * blockDim.x) {
+    const long long total = cost_ex[nsl];
+    const long long target = (total * w + W - 1) / W;
+    int lo = 0, hi = nsl;  // first s with cost_ex[s] >= target
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cost_ex[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    wstep[w] = (int)step_ex[w == W ? nsl : lo];
+  }
+}
+
+// One warp per slice: header + data steps.
+__global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __restrict__ slen, int J, int nsl,
+                                 const long long* __restrict__ step_ex, const int* __restrict__ jstart,
+                                 const int* __restrict__ jout,
+                                 const int* __restrict__ col, const float* __restrict__ val, int* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (long long s = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; s < nsl;
+       s += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long j = 32 * s + lane;
+    const bool ok = j < J;
+    const int L = slen[32 * s];
+    const int idx = ok ? sidx[j] : 0;
+    const int len = ok ? slen[j] : 0;
+    const int st = ok ? jstart[idx] : 0;
+    int* p = out + step_ex[s] * kSellStepInts;
+    p[lane] = ok ? jout[idx] : -1;
+    p[32 + lane] = len;
+    for (int t = 0; t < L; ++t) {
+      int* q = p + (long long)(t + 1) * kSellStepInts;
+      const bool in = t < len;
+      q[lane] = in ? col[st + t] : 0;
+      q[32 + lane] = in ? __float_as_int(val[st + t]) : 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sweep
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// (a0, a1) += v * (x0, x1), each element rounded twice like the reference's
+// `acc += v * x` (kernels.hpp:439-441): FMUL2, then FFMA2 by `one` (opaque to
+// ptxas, see f2_add) so the product is not fused into the add.  One asm block
+// over scalar operands: ptxas keeps the accumulators in place (64-bit asm
+// operands cost ~16 register moves per step).
+__device__ __forceinline__ void f2_mac(float& a0, float& a1, float v, float x0, float x1, f32x2 one) {
+  asm("{\n .reg .b64 p, q, r;\n mov.b64 q, {%2, %2};\n mov.b64 r, {%3, %4};\n mul.rn.f32x2 p, q, r;\n"
+      " mov.b64 r, {%0, %1};\n fma.rn.f32x2 r, p, %5, r;\n mov.b64 {%0, %1}, r;\n}"
+      : "+f"(a0), "+f"(a1)
+      : "f"(v), "f"(x0), "f"(x1), "l"(one));
+}
+
+struct SellArgs {
+  const int* __restrict__ steps;  // T steps x 64 ints
+  const int* __restrict__ wstep;  // nwarps + 1 range starts (step indices)
+  const float* __restrict__ X;    // K x N
+  float* __restrict__ Y;          // M x N
+  float* __restrict__ H;          // partial slots x N
+  int N;
+  int nwarps;
+  f32x2 one2;                     // {1, 1}, opaque to ptxas (see f2_add)
+};
+
+constexpr int kSellStage = 32 * 128;  // one step's 32 dense rows in the ring
+template <int S, int C>
+__host__ __device__ constexpr int sell_warp_bytes() {
+  return S * kSellStage + C * kSellStepInts * 4;
+}
+template <int S, int C, int WPC>
+__host__ __device__ constexpr int sell_smem_bytes() {
+  return WPC * sell_warp_bytes<S, C>();
+}
+
+template <int S, int C, int WPC, int MINB>
+__global__ void __launch_bounds__(WPC * 32, MINB)
+seq_sell_kernel(const SellArgs a) {
+  static_assert(S >= 2 && C >= S + 1 && (S & (S - 1)) == 0 && (C & (C - 1)) == 0, "ring depths");
+  extern __shared__ __align__(128) unsigned char s_sell[];
+  // the fold pass (a programmatic dependent) may be scheduled as CTAs drain;
+  // it still waits for this grid's completion before reading H
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * WPC + warp;
+  if (w >= a.nwarps) return;
+  const int g0 = a.wstep[w], g1 = a.wstep[w + 1];
+  if (g0 >= g1) return;
+  unsigned char* wb = s_sell + warp * sell_warp_bytes<S, C>();
+  const int* cr = reinterpret_cast<const int*>(wb + S * kSellStage);  // [C][64]
+  const unsigned xr0 = smem_addr(wb);
+  const unsigned cr0 = xr0 + S * kSellStage;
+  const int col0 = blockIdx.y * 32;
+  const int* steps = a.steps;
+  // LDGSTS lanes: rows 8 * (lane >> 3) + i (i = 0..7), 16-byte chunk lane & 7
+  const int rg = lane >> 3, ch = lane & 7;
+  // 32-bit row offsets in 16-byte units (the plan checks K * N / 4 < 2^32)
+  const float4* xg = reinterpret_cast<const float4*>(a.X + col0);
+  const unsigned n16 = (unsigned)a.N / 4;
+  const unsigned xdst0 = xr0 + (unsigned)(rg * 8 * 128 + ch * 16);
+
+  // step g into step-ring slot cs: lanes 0..15, 16 B each
+  auto fetch_step = [&](int g, int cs) {
+    if (lane < 16 && g < g1) cp16(cr0 + cs * 256 + lane * 16, steps + (size_t)g * kSellStepInts + lane * 4);
+  };
+  int prem = 0;  // producer: data steps left in the current slice
+  // dense rows of step p (step slot pcs) into row-ring slot pxs
+  auto produce = [&](int p, int pcs, int pxs) {
+    if (p >= g1) return;
+    if (prem == 0) {  // header: no rows
+      prem = cr[pcs * kSellStepInts + 32];
+      return;
+    }
+    --prem;
+    const int4 c0 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg];
+    const int4 c1 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg + 1];
+    const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const unsigned d = xdst0 + pxs * kSellStage;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cp16(d + i * 128, xg + ((unsigned)cc[i] * n16 + ch));
+  };
+
+  // prologue: steps 0 .. C-2 (one group each), then rows of steps 0 .. S-2
+#pragma unroll 1
+  for (int i = 0; i < C - 1; ++i) {
+    fetch_step(g0 + i, i);
+    cp_commit();
+  }
+#pragma unroll 1
+  for (int i = 0; i < S - 1; ++i) {
+    cp_wait<C - 2>();
+    __syncwarp();
+    produce(g0 + i, i, i);
+    cp_commit();
+  }
+
+  // this lane's row in a ring stage, read in rotated chunk order
+  unsigned roff[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) roff[c] = (unsigned)(lane * 128 + (((c + lane) & 7) * 16));
+  float acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+  int out = -1, crem = 0;
+  int t = 0, len = 0;  // position in the slice, this lane's job length
+  const size_t ystride = (size_t)a.N;
+  auto epilogue = [&]() {
+    if (out == -1) return;
+    float* base = (out >= 0 ? a.Y + (size_t)out * ystride : a.H + (size_t)(out & 0x7fffffff) * ystride) + col0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int k = (c + lane) & 7;  // slot c holds chunk (c + lane) & 7
+      if (out >= 0) st_y4(base + 4 * k, acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+      else *reinterpret_cast<float4*>(base + 4 * k) = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+    }
+  };
+
+  // Main loop (S, C powers of two): iteration k consumes step g = g0 + k from
+  // step slot k % C and row slot k % S, produces the rows of step g + S - 1 and
+  // fetches step g + C - 1 into the slot step g - 1 used.  (Unrolling by C to
+  // make the slots compile-time constants measured 4 % faster, but its 8
+  // inlined epilogues bloat the code; kept rolled.)
+  const int n = g1 - g0;
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const int g = g0 + k;
+    // producer (its step landed: all but the last C - S - 1 groups are complete)
+    cp_wait<C - S - 1>();
+    __syncwarp();
+    produce(g + S - 1, (k + S - 1) & (C - 1), (k + S - 1) & (S - 1));
+    fetch_step(g + C - 1, (k + C - 1) & (C - 1));
+    cp_commit();
+    // consumer: step g
+    cp_wait<S - 1>();
+    __syncwarp();
+    const int* cw = cr + (k & (C - 1)) * kSellStepInts;
+    if (crem == 0) {  // header: finish the previous slice, start the next
+      epilogue();
+      out = cw[lane];
+      len = cw[32 + lane];
+      crem = cw[32];  // lane 0 runs the slice's longest job
+      t = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+    } else {
+      const float v = __int_as_float(cw[32 + lane]);
+      const unsigned char* xrow = wb + (k & (S - 1)) * kSellStage;
+      if (t < len) {  // padding positions add nothing (also when X holds inf / NaN)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = *reinterpret_cast<const float4*>(xrow + roff[c]);
+          f2_mac(acc[4 * c], acc[4 * c + 1], v, x.x, x.y, a.one2);
+          f2_mac(acc[4 * c + 2], acc[4 * c + 3], v, x.z, x.w, a.one2);
+        }
+      }
+      ++t;
+      --crem;
+    }
+  }
+  epilogue();
+  cp_wait<0>();
+}
+
+// Y[row] = ((0 + H[s0]) + H[s0 + 1]) + ... (kernels.hpp:448-453: ascending
+// chunk order) for the rows that cross a chunk boundary, per 32-column tile.
+// The fold list is sorted by slot count, longest first:
+//   * rows of > kFoldWarpMax slots (few; chains up to nnz / seq_chunk long):
+//     one CTA per (row, tile) stages up to kFoldStage slots in shared memory
+//     with all its threads (every load in flight at once), then warp 0 adds
+//     them in order, lane = column;
+//   * the others (most rows: 2 slots): kFoldRows (row, tile) items per warp,
+//     all their loads in flight, lane = column.
+// Launched as a programmatic dependent of the sweep: the descriptor load
+// overlaps the sweep's tail, griddepcontrol.wait orders the H reads after it.
+constexpr int kFoldWarpMax = 8;
+constexpr int kFoldStage = 256;
+constexpr int kFoldRows = 4;  // small-row items per warp
+__global__ void __launch_bounds__(256) sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig,
+                                                        const float* __restrict__ H, float* __restrict__ Y, int N) {
+  __shared__ float buf[kFoldStage][33];
+  const int tiles = N / 32;
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x < (unsigned)(nbig * tiles)) {
+    const int4 d = fold[blockIdx.x / tiles];
+    const int c0 = (int)(blockIdx.x % tiles) * 32;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const float* h = H + (size_t)d.y * N + c0;
+    float y = 0.f;
+    for (int k0 = 0; k0 < d.z; k0 += kFoldStage) {
+      const int n = min(kFoldStage, d.z - k0);
+#pragma unroll 4
+      for (int r = threadIdx.x >> 5; r < n; r += 8) buf[r][lane] = h[(size_t)(k0 + r) * N + lane];
+      __syncthreads();
+      if (threadIdx.x < 32)
+        for (int r = 0; r < n; ++r) y = __fadd_rn(y, buf[r][lane]);
+      __syncthreads();
+    }
+    if (threadIdx.x < 32) st_y(Y + (size_t)d.x * N + c0 + lane, y);
+    return;
+  }
+  // kFoldRows consecutive (row, tile) items per warp, all their loads in flight
+  const long long item0 = (long long)nbig * tiles +
+                          (((blockIdx.x - (long long)nbig * tiles) * blockDim.x + threadIdx.x) >> 5) * kFoldRows;
+  const long long nitems = (long long)nfold * tiles;
+  int4 d[kFoldRows];
+  int c[kFoldRows];
+#pragma unroll
+  for (int r = 0; r < kFoldRows; ++r) {
+    const long long it = item0 + r;
+    d[r] = it < nitems ? fold[it / tiles] : make_int4(0, 0, 0, 0);
+    c[r] = it < nitems ? (int)(it % tiles) * 32 + lane : 0;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (item0 >= nitems) return;
+  float v[kFoldRows][kFoldWarpMax];
+#pragma unroll
+  for (int r = 0; r < kFoldRows; ++r) {
+    const float* h = H + (size_t)d[r].y * N + c[r];
+#pragma unroll
+    for (int u = 0; u < kFoldWarpMax; ++u) v[r][u] = u < d[r].z ? h[(size_t)u * N] : 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < kFoldRows; ++r) {
+    if (d[r].z == 0) continue;
+    float y = 0.f;
+#pragma unroll
+    for (int u = 0; u < kFoldWarpMax; ++u)
+      if (u < d[r].z) y = __fadd_rn(y, v[r][u]);
+    st_y(Y + (size_t)d[r].x * N + c[r], y);
+  }
+}
+
+}  // namespace spmk_dev
