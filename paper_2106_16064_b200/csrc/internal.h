@@ -102,7 +102,9 @@ struct SellPlan {
   int shape = 0;            // sweep shape (launch_sell.cu kSellShapes)
   int* steps = nullptr;     // nsteps x 64 ints
   long long nsteps = 0;
-  int* wstep = nullptr;     // nwarps + 1 range starts
+  int* cstep = nullptr;     // nchunks + 1 work-queue chunk starts (step indices)
+  int nchunks = 0;
+  int* sched = nullptr;     // per column tile {claim counter, warps done}
   int nwarps = 0, blocks = 0;
   int4* fold = nullptr;     // {row, first slot, slots} of the rows of >= 3 segments
   int nfold = 0;

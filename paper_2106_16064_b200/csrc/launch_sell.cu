@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <map>
 #include <mutex>
@@ -16,6 +17,8 @@ using namespace spmk_dev;
 namespace spmk_host {
 namespace {
 
+constexpr int kSellChunkMin = 16, kSellChunkMax = 512;  // work-queue chunk sizes (steps; >= C)
+constexpr int kSellMaxTiles = 64;                        // column tiles (N <= 2048)
 // Sweep shapes (ring depths S / C, warps per CTA, CTAs per SM); tuning knob
 // sell_cfg picks one (measured on B200).
 struct SellShape {
@@ -93,12 +96,38 @@ int sell_shape_of(const spmk_csr_s* h) {
   return v >= 0 && v < kSellShapeCount ? (int)v : 0;
 }
 
+// Dev tracing (SPMK_SELL_TRACE=1): per-warp start / end times of the last
+// sweep, read back with spmk_sell_trace (not part of the drop-in surface).
+unsigned long long* g_trace = nullptr;
+int g_trace_n = 0;
+unsigned long long* sell_trace_buffer(int nwarps) {
+  static const bool on = [] {
+    const char* v = std::getenv("SPMK_SELL_TRACE");
+    return v && *v == '1';
+  }();
+  if (!on) return nullptr;
+  if (g_trace_n < nwarps) {
+    cudaFree(g_trace);
+    g_trace = dev_alloc<unsigned long long>((size_t)4 * nwarps);
+    g_trace_n = nwarps;
+  }
+  return g_trace;
+}
+
 }  // namespace
+
+extern "C" int spmk_sell_trace(unsigned long long* out, int cap) {
+  const int n = std::min(cap, g_trace_n);
+  if (n > 0 && cudaMemcpy(out, g_trace, sizeof(unsigned long long) * 4 * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return n;
+}
 
 bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned) {
   // N = 32 only: at N = 64 / 128 the tile sweep (16 / 32 lanes per unit,
   // 256 / 512-byte rows per gather) measured 7 % / 34 % faster on B200
-  const bool shape_ok = h->tune.seq_impl == 2 ? N == 32 : (h->tune.seq_impl == 3 && N % 32 == 0);
+  const bool shape_ok =
+      h->tune.seq_impl == 2 ? N == 32 : (h->tune.seq_impl == 3 && N % 32 == 0 && N / 32 <= kSellMaxTiles);
   return shape_ok && aligned && CH <= kSellMaxChunk && h->k < INT32_MAX &&
          (unsigned long long)h->k * (unsigned long long)(N / 4) < (1ull << 32) &&
          h->nnz < INT32_MAX && h->m < INT32_MAX;
@@ -168,15 +197,14 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
     CK(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, jlen.p, slen.p, idx.p, sidx.p, J, 0, 16, s));
   }
   const int nsl = (J + 31) / 32;
-  DevTmp<long long> lsteps(nsl + 1), lcost(nsl + 1), step_ex(nsl + 1), cost_ex(nsl + 1);
+  DevTmp<long long> lsteps(nsl + 1), lcost(nsl + 1), step_ex(nsl + 1);
   CK(cudaMemsetAsync(lsteps.p + nsl, 0, sizeof(long long), s));
-  CK(cudaMemsetAsync(lcost.p + nsl, 0, sizeof(long long), s));
   sell_slice_kernel<<<grid_for(nsl), 256, 0, s>>>(slen.p, nsl, lsteps.p, lcost.p); LAUNCHED(1);
   exclusive_scan(lsteps.p, step_ex.p, nsl + 1, s);
-  exclusive_scan(lcost.p, cost_ex.p, nsl + 1, s);
-  long long T = 0;
-  CK(cudaMemcpyAsync(&T, step_ex.p + nsl, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  std::vector<long long> sx((size_t)nsl + 1);
+  CK(cudaMemcpyAsync(sx.data(), step_ex.p, sizeof(long long) * sx.size(), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  const long long T = sx[(size_t)nsl];
   if (T >= INT32_MAX) throw CudaError{SPMK_EUNSUPPORTED, "sell layout: too many steps"};
   p.nsteps = T;
   p.steps = dev_alloc<int>((size_t)T * kSellStepInts);
@@ -185,18 +213,37 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   p.blocks = sms * sell_blocks_per_sm(shape);
   p.nwarps = p.blocks * kSellShapes[shape].wpc;
-  p.wstep = dev_alloc<int>((size_t)p.nwarps + 1);
-  sell_ranges_kernel<<<grid_for(p.nwarps + 1), 256, 0, s>>>(cost_ex.p, step_ex.p, nsl, p.nwarps, p.wstep); LAUNCHED(1);
+  // Chunks of whole slices for the warps' work queue, guided sizes: about
+  // remaining / (4 W) steps, clamped to [kSellChunkMin, kSellChunkMax] (a
+  // slice longer than that is one chunk); the first W are the warps' first
+  // chunks, the rest are claimed in order.
+  std::vector<int> cs;
+  cs.reserve(4 * (size_t)p.nwarps + 16);
+  int si = 0;
+  while (si < nsl) {
+    cs.push_back((int)sx[(size_t)si]);
+    const long long rem = T - sx[(size_t)si];
+    const long long target = std::max<long long>(kSellChunkMin, std::min<long long>(kSellChunkMax, rem / (4LL * p.nwarps)));
+    const long long start = sx[(size_t)si];
+    while (si < nsl && sx[(size_t)si] - start < target) ++si;
+  }
+  cs.push_back((int)T);
+  p.nchunks = (int)cs.size() - 1;
+  p.cstep = dev_alloc<int>(cs.size());
+  CK(cudaMemcpyAsync(p.cstep, cs.data(), sizeof(int) * cs.size(), cudaMemcpyHostToDevice, s));
+  p.sched = dev_alloc<int>(2 * kSellMaxTiles);
+  CK(cudaMemsetAsync(p.sched, 0, sizeof(int) * 2 * kSellMaxTiles, s));
   sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, step_ex.p, jstart.p, jout.p,
                                                                  h->col, h->val, p.steps); LAUNCHED(1);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(s));  // temporaries are freed on return
+  CK(cudaStreamSynchronize(s));  // temporaries (and cs) are freed on return
   return h->sell_plans.emplace(std::make_pair(CH, shape), p).first->second;
 }
 
 void free_sell_plan(SellPlan& p) {
   cudaFree(p.steps);
-  cudaFree(p.wstep);
+  cudaFree(p.cstep);
+  cudaFree(p.sched);
   cudaFree(p.fold);
   p = SellPlan{};
 }
@@ -205,13 +252,15 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
   const int tiles = N / 32;
   SellArgs a{};
   a.steps = p.steps;
-  a.wstep = p.wstep;
+  a.cstep = p.cstep;
+  a.sched = p.sched;
+  a.nchunks = p.nchunks;
   a.X = X;
   a.Y = Y;
   a.H = H;
   a.N = N;
-  a.nwarps = p.nwarps;
   a.one2 = kOnePair;
+  a.trace = sell_trace_buffer(p.nwarps);
   sell_blocks_per_sm(p.shape);  // shared-memory opt-in on this device
   kSellShapes[p.shape].launch(dim3(p.blocks, tiles), a, s); LAUNCHED(1);
   if (p.nfold > 0) {

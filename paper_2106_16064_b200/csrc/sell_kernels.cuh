@@ -29,8 +29,10 @@
 //   data:   [lane] = column (0 for padding), [32 + lane] = value bits (0 for padding)
 // Padding positions (t >= the lane's job length) gather row 0 and are not added.
 //
-// Sweep (seq_sell_kernel): persistent warps, each over a contiguous range of
-// steps balanced at plan time.  Per warp, in shared memory, filled with
+// Sweep (seq_sell_kernel): persistent warps pulling chunks of whole slices
+// (heaviest first, sizes shrinking toward the end) from an atomic counter —
+// static per-warp ranges left the slowest warp at 1.6x the median (the
+// per-step time varies with the rows' L2 hit rates).  Per warp, in shared memory, filled with
 // cp.async (LDGSTS, 16 B per lane, one commit group per iteration):
 //   * a C-stage ring of steps, C - 1 steps ahead of the consumer;
 //   * an S-stage ring of dense rows, S - 1 steps ahead: 8 LDGSTS per step,
@@ -118,23 +120,6 @@ __global__ void sell_slice_kernel(const int* __restrict__ slen_sorted, int nsl, 
   }
 }
 
-// First step of every warp's range: the first slice whose cost prefix reaches
-// w * total / W (contiguous ranges, cut at slice boundaries).
-__global__ void sell_ranges_kernel(const long long* __restrict__ cost_ex, const long long* __restrict__ step_ex,
-                                   int nsl, int W, int* __restrict__ wstep) {
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= W; w += gridDim.x * blockDim.x) {
-    const long long total = cost_ex[nsl];
-    const long long target = (total * w + W - 1) / W;
-    int lo = 0, hi = nsl;  // first s with cost_ex[s] >= target
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (cost_ex[mid] < target) lo = mid + 1;
-      else hi = mid;
-    }
-    wstep[w] = (int)step_ex[w == W ? nsl : lo];
-  }
-}
-
 // One warp per slice: header + data steps.
 __global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __restrict__ slen, int J, int nsl,
                                  const long long* __restrict__ step_ex, const int* __restrict__ jstart,
@@ -185,13 +170,15 @@ __device__ __forceinline__ void f2_mac(float& a0, float& a1, float v, float x0, 
 
 struct SellArgs {
   const int* __restrict__ steps;  // T steps x 64 ints
-  const int* __restrict__ wstep;  // nwarps + 1 range starts (step indices)
+  const int* __restrict__ cstep;  // nchunks + 1 chunk starts (step indices; whole slices, heaviest first)
+  int* __restrict__ sched;        // per column tile {claim counter, warps done}, zero between calls
+  int nchunks;
   const float* __restrict__ X;    // K x N
   float* __restrict__ Y;          // M x N
   float* __restrict__ H;          // partial slots x N
   int N;
-  int nwarps;
   f32x2 one2;                     // {1, 1}, opaque to ptxas (see f2_add)
+  unsigned long long* trace;      // dev: per-warp {start, end, steps, slices} (%globaltimer), or null
 };
 
 constexpr int kSellStage = 32 * 128;  // one step's 32 dense rows in the ring
@@ -214,9 +201,12 @@ seq_sell_kernel(const SellArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * WPC + warp;
-  if (w >= a.nwarps) return;
-  const int g0 = a.wstep[w], g1 = a.wstep[w + 1];
-  if (g0 >= g1) return;
+  const int W = gridDim.x * WPC;
+  int* sched = a.sched + 2 * blockIdx.y;  // {chunks claimed beyond the first W, warps done}
+  unsigned long long t_start = 0;
+  int nsteps = 0, nslices = 0;
+  if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+
   unsigned char* wb = s_sell + warp * sell_warp_bytes<S, C>();
   const int* cr = reinterpret_cast<const int*>(wb + S * kSellStage);  // [C][64]
   const unsigned xr0 = smem_addr(wb);
@@ -230,14 +220,51 @@ seq_sell_kernel(const SellArgs a) {
   const unsigned n16 = (unsigned)a.N / 4;
   const unsigned xdst0 = xr0 + (unsigned)(rg * 8 * 128 + ch * 16);
 
+  // Work: chunks of whole slices (plan: a.cstep), heaviest first.  Warp w
+  // starts with chunk w and claims the next one (atomic counter) as soon as
+  // it enters a chunk; the claim and the chunk bounds load are consumed only
+  // when the step ring reaches the chunk end (every chunk but the last has
+  // >= C steps, so the rings never run more than one chunk ahead).
+  int a0 = 0, alen = 0;                   // chunk the consumer is in (real start, steps)
+  int b0 = 0, blen = 0, bknown = 1;       // next chunk (bknown = 0: claim in flight)
+  int pc0 = 0, pc1 = 0;                   // lane 0: the claim's bounds
+  auto claim = [&]() {
+    if (lane == 0) {
+      const int c = atomicAdd(sched, 1) + W;
+      pc0 = c < a.nchunks ? a.cstep[c] : 0;
+      pc1 = c < a.nchunks ? a.cstep[c + 1] : 0;
+    }
+    bknown = 0;
+  };
+  auto resolve = [&]() {
+    if (!bknown) {
+      b0 = __shfl_sync(0xffffffffu, pc0, 0);
+      blen = __shfl_sync(0xffffffffu, pc1, 0) - b0;
+      bknown = 1;
+    }
+  };
+  // real step at virtual position v of the consumer's chunk (-1: none)
+  auto map = [&](int v) -> int {
+    if (v < alen) return a0 + v;
+    resolve();
+    return v - alen < blen ? b0 + (v - alen) : -1;
+  };
+  if (w < a.nchunks) {
+    a0 = a.cstep[w];
+    alen = a.cstep[w + 1] - a0;
+    claim();
+  } else {
+    blen = 0;
+  }
+
   // step g into step-ring slot cs: lanes 0..15, 16 B each
   auto fetch_step = [&](int g, int cs) {
-    if (lane < 16 && g < g1) cp16(cr0 + cs * 256 + lane * 16, steps + (size_t)g * kSellStepInts + lane * 4);
+    if (lane < 16 && g >= 0) cp16(cr0 + cs * 256 + lane * 16, steps + (size_t)g * kSellStepInts + lane * 4);
   };
   int prem = 0;  // producer: data steps left in the current slice
   // dense rows of step p (step slot pcs) into row-ring slot pxs
   auto produce = [&](int p, int pcs, int pxs) {
-    if (p >= g1) return;
+    if (p < 0) return;
     if (prem == 0) {  // header: no rows
       prem = cr[pcs * kSellStepInts + 32];
       return;
@@ -254,14 +281,14 @@ seq_sell_kernel(const SellArgs a) {
   // prologue: steps 0 .. C-2 (one group each), then rows of steps 0 .. S-2
 #pragma unroll 1
   for (int i = 0; i < C - 1; ++i) {
-    fetch_step(g0 + i, i);
+    fetch_step(map(i), i);
     cp_commit();
   }
 #pragma unroll 1
   for (int i = 0; i < S - 1; ++i) {
     cp_wait<C - 2>();
     __syncwarp();
-    produce(g0 + i, i, i);
+    produce(map(i), i, i);
     cp_commit();
   }
 
@@ -286,26 +313,33 @@ seq_sell_kernel(const SellArgs a) {
     }
   };
 
-  // Main loop (S, C powers of two): iteration k consumes step g = g0 + k from
-  // step slot k % C and row slot k % S, produces the rows of step g + S - 1 and
-  // fetches step g + C - 1 into the slot step g - 1 used.  (Unrolling by C to
-  // make the slots compile-time constants measured 4 % faster, but its 8
-  // inlined epilogues bloat the code; kept rolled.)
-  const int n = g1 - g0;
+  // Main loop (S, C powers of two): iteration it consumes the step at virtual
+  // position k from step slot it % C and row slot it % S, produces the rows
+  // of position k + S - 1 and fetches position k + C - 1 into the slot the
+  // previous iteration consumed.
+  int k = 0;
 #pragma unroll 1
-  for (int k = 0; k < n; ++k) {
-    const int g = g0 + k;
+  for (int it = 0;; ++it) {
+    if (k == alen) {  // the consumer leaves its chunk
+      resolve();
+      if (blen <= 0) break;
+      a0 = b0;
+      alen = blen;
+      k = 0;
+      claim();
+    }
     // producer (its step landed: all but the last C - S - 1 groups are complete)
     cp_wait<C - S - 1>();
     __syncwarp();
-    produce(g + S - 1, (k + S - 1) & (C - 1), (k + S - 1) & (S - 1));
-    fetch_step(g + C - 1, (k + C - 1) & (C - 1));
+    produce(map(k + S - 1), (it + S - 1) & (C - 1), (it + S - 1) & (S - 1));
+    fetch_step(map(k + C - 1), (it + C - 1) & (C - 1));
     cp_commit();
-    // consumer: step g
+    // consumer
     cp_wait<S - 1>();
     __syncwarp();
-    const int* cw = cr + (k & (C - 1)) * kSellStepInts;
+    const int* cw = cr + (it & (C - 1)) * kSellStepInts;
     if (crem == 0) {  // header: finish the previous slice, start the next
+      ++nslices;
       epilogue();
       out = cw[lane];
       len = cw[32 + lane];
@@ -315,7 +349,7 @@ seq_sell_kernel(const SellArgs a) {
       for (int c = 0; c < 32; ++c) acc[c] = 0.f;
     } else {
       const float v = __int_as_float(cw[32 + lane]);
-      const unsigned char* xrow = wb + (k & (S - 1)) * kSellStage;
+      const unsigned char* xrow = wb + (it & (S - 1)) * kSellStage;
       if (t < len) {  // padding positions add nothing (also when X holds inf / NaN)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -327,9 +361,28 @@ seq_sell_kernel(const SellArgs a) {
       ++t;
       --crem;
     }
+    ++k;
+    ++nsteps;
   }
   epilogue();
   cp_wait<0>();
+  if (lane == 0) {
+    // the last warp out resets the counters for the next call
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == W - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+    if (a.trace && blockIdx.y == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      a.trace[4 * w] = t_start;
+      a.trace[4 * w + 1] = t_end;
+      a.trace[4 * w + 2] = (unsigned long long)nsteps;
+      a.trace[4 * w + 3] = (unsigned long long)nslices;
+    }
+  }
 }
 
 // Y[row] = ((0 + H[s0]) + H[s0 + 1]) + ... (kernels.hpp:448-453: ascending
