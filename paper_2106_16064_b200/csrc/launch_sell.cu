@@ -267,8 +267,9 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
     // programmatic dependent launch: scheduled while the sweep drains
     cudaLaunchConfig_t lc = {};
     const long long small_warps = ((long long)(p.nfold - p.nbig) * tiles + kFoldRows - 1) / kFoldRows;
-    lc.gridDim = dim3((unsigned)((long long)p.nbig * tiles + (small_warps + 7) / 8));
-    lc.blockDim = dim3(256);
+    constexpr int wpb = kFoldThreads / 32;
+    lc.gridDim = dim3((unsigned)((long long)p.nbig * tiles + (small_warps + wpb - 1) / wpb));
+    lc.blockDim = dim3(kFoldThreads);
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -397,42 +397,63 @@ seq_sell_kernel(const SellArgs a) {
 // Launched as a programmatic dependent of the sweep: the descriptor load
 // overlaps the sweep's tail, griddepcontrol.wait orders the H reads after it.
 constexpr int kFoldWarpMax = 8;
-constexpr int kFoldStage = 256;
-constexpr int kFoldRows = 4;  // small-row items per warp
-__global__ void __launch_bounds__(256) sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig,
-                                                        const float* __restrict__ H, float* __restrict__ Y, int N) {
+constexpr int kFoldStage = 64;    // slots staged per round of a long row
+constexpr int kFoldRows = 4;      // short-row items per warp
+constexpr int kFoldThreads = 64;  // 2 warps per block: small blocks, many resident
+__global__ void __launch_bounds__(kFoldThreads, 16)
+sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float* __restrict__ H,
+                 float* __restrict__ Y, int N) {
+  constexpr int WPB = kFoldThreads / 32;
   __shared__ float buf[kFoldStage][33];
-  const int tiles = N / 32;
-  const int lane = threadIdx.x & 31;
-  if (blockIdx.x < (unsigned)(nbig * tiles)) {
-    const int4 d = fold[blockIdx.x / tiles];
-    const int c0 = (int)(blockIdx.x % tiles) * 32;
+  const int tiles = N >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nbig_items = nbig * tiles;
+  if ((int)blockIdx.x < nbig_items) {
+    const int f = (int)blockIdx.x / tiles;
+    const int c0 = ((int)blockIdx.x - f * tiles) * 32;
+    const int4 d = fold[f];
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const float* h = H + (size_t)d.y * N + c0;
+    const float* h = H + (size_t)d.y * N + c0 + lane;
     float y = 0.f;
     for (int k0 = 0; k0 < d.z; k0 += kFoldStage) {
       const int n = min(kFoldStage, d.z - k0);
-#pragma unroll 4
-      for (int r = threadIdx.x >> 5; r < n; r += 8) buf[r][lane] = h[(size_t)(k0 + r) * N + lane];
+      // every load of the round in flight at once: slot r = warp + WPB u
+      float tmp[kFoldStage / WPB];
+#pragma unroll
+      for (int u = 0; u < kFoldStage / WPB; ++u) {
+        const int r = warp + WPB * u;
+        tmp[u] = r < n ? h[(size_t)(k0 + r) * N] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kFoldStage / WPB; ++u) buf[warp + WPB * u][lane] = tmp[u];
       __syncthreads();
-      if (threadIdx.x < 32)
-        for (int r = 0; r < n; ++r) y = __fadd_rn(y, buf[r][lane]);
+      if (warp == 0) {
+        int r = 0;
+        for (; r + 8 <= n; r += 8) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = buf[r + e][lane];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) y = __fadd_rn(y, v[e]);
+        }
+        for (; r < n; ++r) y = __fadd_rn(y, buf[r][lane]);
+      }
       __syncthreads();
     }
-    if (threadIdx.x < 32) st_y(Y + (size_t)d.x * N + c0 + lane, y);
+    if (warp == 0) st_y(Y + (size_t)d.x * N + c0 + lane, y);
     return;
   }
   // kFoldRows consecutive (row, tile) items per warp, all their loads in flight
-  const long long item0 = (long long)nbig * tiles +
-                          (((blockIdx.x - (long long)nbig * tiles) * blockDim.x + threadIdx.x) >> 5) * kFoldRows;
-  const long long nitems = (long long)nfold * tiles;
+  const int item0 = nbig_items + (((int)blockIdx.x - nbig_items) * WPB + warp) * kFoldRows;
+  const int nitems = nfold * tiles;
   int4 d[kFoldRows];
   int c[kFoldRows];
 #pragma unroll
   for (int r = 0; r < kFoldRows; ++r) {
-    const long long it = item0 + r;
-    d[r] = it < nitems ? fold[it / tiles] : make_int4(0, 0, 0, 0);
-    c[r] = it < nitems ? (int)(it % tiles) * 32 + lane : 0;
+    const int it = item0 + r;
+    const int f = tiles == 1 ? it : it / tiles;
+    d[r] = it < nitems ? fold[f] : make_int4(0, 0, 0, 0);
+    c[r] = (it - f * tiles) * 32 + lane;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (item0 >= nitems) return;
