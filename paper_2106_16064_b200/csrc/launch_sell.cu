@@ -37,7 +37,7 @@ constexpr SellShape sell_shape() {
 }
 const SellShape kSellShapes[] = {
     sell_shape<4, 8, 4, 3>(),   // 0: 12 warps / SM, 3 steps of rows in flight per warp
-    sell_shape<2, 8, 8, 2>(),   // 1: 16 warps, 1 in flight
+    sell_shape<2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
     sell_shape<4, 8, 12, 1>(),  // 2: 12 warps in one CTA
     sell_shape<8, 16, 3, 2>(),  // 3: 6 warps, 7 in flight
 };

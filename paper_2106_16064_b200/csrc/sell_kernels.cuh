@@ -194,7 +194,7 @@ __host__ __device__ constexpr int sell_smem_bytes() {
 template <int S, int C, int WPC, int MINB>
 __global__ void __launch_bounds__(WPC * 32, MINB)
 seq_sell_kernel(const SellArgs a) {
-  static_assert(S >= 2 && C >= S + 1 && (S & (S - 1)) == 0 && (C & (C - 1)) == 0, "ring depths");
+  static_assert(S >= 2 && C >= 2 * S - 1 && (S & (S - 1)) == 0 && (C & (C - 1)) == 0, "ring depths");
   extern __shared__ __align__(128) unsigned char s_sell[];
   // the fold pass (a programmatic dependent) may be scheduled as CTAs drain;
   // it still waits for this grid's completion before reading H
@@ -315,7 +315,7 @@ seq_sell_kernel(const SellArgs a) {
 
   // Main loop (S, C powers of two): iteration it consumes the step at virtual
   // position k from step slot it % C and row slot it % S, produces the rows
-  // of position k + S - 1 and fetches position k + C - 1 into the slot the
+  // of position k + S - 1 and fetches position k + C - 1 into the slots the
   // previous iteration consumed.
   int k = 0;
 #pragma unroll 1
@@ -328,15 +328,29 @@ seq_sell_kernel(const SellArgs a) {
       k = 0;
       claim();
     }
-    // producer (its step landed: all but the last C - S - 1 groups are complete)
-    cp_wait<C - S - 1>();
+    // One wait per iteration: all but the last S - 2 cp.async groups are
+    // complete, i.e. the rows of position k (issued S - 1 iterations ago) and
+    // the step of position k + S - 1 (fetched C - 1 steps ahead, C >= 2S - 1).
+    cp_wait<S - 2>();
     __syncwarp();
-    produce(map(k + S - 1), (it + S - 1) & (C - 1), (it + S - 1) & (S - 1));
-    fetch_step(map(k + C - 1), (it + C - 1) & (C - 1));
-    cp_commit();
-    // consumer
-    cp_wait<S - 1>();
-    __syncwarp();
+    // producer, part 1: the columns of position k + S - 1 (smem loads issued
+    // now, consumed after the consumer's work)
+    const int p = map(k + S - 1);
+    const int pcs = (it + S - 1) & (C - 1);
+    bool issue = false;
+    int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
+    if (p >= 0) {
+      if (prem == 0) {  // header: no rows
+        prem = cr[pcs * kSellStepInts + 32];
+      } else {
+        --prem;
+        issue = true;
+        c0 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg];
+        c1 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg + 1];
+      }
+    }
+    const int f = map(k + C - 1);
+    // consumer: position k
     const int* cw = cr + (it & (C - 1)) * kSellStepInts;
     if (crem == 0) {  // header: finish the previous slice, start the next
       ++nslices;
@@ -361,6 +375,16 @@ seq_sell_kernel(const SellArgs a) {
       ++t;
       --crem;
     }
+    // producer, part 2: rows of position k + S - 1 into the row slot, and the
+    // step of position k + C - 1 into the step slot, that position k - 1 used
+    if (issue) {
+      const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const unsigned d = xdst0 + ((it + S - 1) & (S - 1)) * kSellStage;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cp16(d + i * 128, xg + ((unsigned)cc[i] * n16 + ch));
+    }
+    fetch_step(f, (it + C - 1) & (C - 1));
+    cp_commit();
     ++k;
     ++nsteps;
   }
