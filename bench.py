@@ -401,7 +401,12 @@ def run_workload(wl, args, ranks: Ranks, local: int, steps: int, e2e: bool, roof
     if roofline and a.num_rows:
         M, nnz = a.num_rows, a.nnz
         m_ne = M - a.empty_rows
-        alg_bytes = 4 * (M + 1) + 8 * nnz + 4 * K * n + 4 * m_ne * n  # empty-row zero-fill: separate kernel
+        path = a.spmm_path(kid, n)
+        # lane-per-job seq-ws: the sweep writes every row of Y (empty rows too)
+        # and the timed region is sweep + fold pass; otherwise the empty-row
+        # zero-fill is a separate side-stream kernel outside the timed region
+        y_rows = M if path == "sell" else m_ne
+        alg_bytes = 4 * (M + 1) + 8 * nnz + 4 * K * n + 4 * y_rows * n
         main_avg_ms = statistics.mean(main_ms)
         achieved = alg_bytes / (main_avg_ms * 1e-3) / 1e9
         peak, peak_kind = peaks()
@@ -413,12 +418,16 @@ def run_workload(wl, args, ranks: Ranks, local: int, steps: int, e2e: bool, roof
             pass
         out["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                           "kernel": f"{spmk.kernel_name(kid)} (dominant launch, avg {main_avg_ms * 1e3:.1f} us"
+                           "kernel": f"{spmk.kernel_name(kid)} ("
+                                     + ("lane-per-job sweep + fold pass" if path == "sell" else "dominant launch")
+                                     + f", avg {main_avg_ms * 1e3:.1f} us"
                                      + (f", rank {rank}" if G > 1 else "") + ")",
                            "algorithmic_bytes_per_launch": int(alg_bytes),
                            "l2_gather_bytes_per_launch": int(nnz * ((4 * n + 127) // 128) * 128),
+                           # vs the measured ceiling of 128-B row gathers with R-MAT column
+                           # statistics (11.4 TB/s, profiles/r02e_microbench_gather.txt)
                            "l2_gather_frac": round(nnz * ((4 * n + 127) // 128) * 128 / (main_avg_ms * 1e-3)
-                                                   / 9.4e12, 4)}
+                                                   / 11.4e12, 4)}
     return out
 
 

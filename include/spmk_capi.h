@@ -234,6 +234,13 @@ uint64_t spmk_launch_count(void);
  * synchronizes on them and returns milliseconds.  For bench.py's roofline. */
 spmk_status spmk_timing_enable(int on);
 spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms);
+/* Which device path spmk_spmm takes for (a, id, cfg, n) with 16-byte aligned
+ * operands: *path = 1 for seq-ws through the lane-per-job sweep + fold pass
+ * (sell_kernels.cuh; empty rows written in the sweep), 0 for the tile /
+ * row-split kernels (empty rows zero-filled by a side-stream kernel).  For
+ * bench.py's roofline bookkeeping (no reference counterpart). */
+spmk_status spmk_spmm_path(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg, int64_t n,
+                           int* path);
 
 /* ------------------------------------------------------------ iterative SpMV */
 /* PageRank-style driver support (BASELINE cfg5; no reference counterpart —

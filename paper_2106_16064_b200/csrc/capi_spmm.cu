@@ -434,4 +434,15 @@ spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms) {
   return SPMK_OK;
 }
 
+spmk_status spmk_spmm_path(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_config* cfg, int64_t n,
+                           int* path) {
+  if (!a || !path) return fail(SPMK_EINVAL, "null argument");
+  const spmk_kernel_config c = cfg_or_default(cfg);
+  *path = (id == SPMK_SEQ_BALANCED && n > 0 && n <= INT32_MAX &&
+           spmk_host::sell_eligible(a, (long long)c.seq_chunk, (int)n, true))
+              ? 1
+              : 0;
+  return SPMK_OK;
+}
+
 }  // extern "C"

@@ -57,6 +57,7 @@ class _Feat(C.Structure):
 
 _SIGS = {
     "spmk_last_error": ([], C.c_char_p),
+    "spmk_spmm_path": ([vp, C.c_int, P(_Cfg), i64, P(C.c_int)], C.c_int),
     "spmk_version": ([], C.c_int),
     "spmk_default_config": ([P(_Cfg)], None),
     "spmk_default_thresholds": ([P(_Thr)], None),
@@ -360,6 +361,14 @@ class DeviceCsr:
     def set_tuning(self, key: str, value: int) -> None:
         """Per-handle performance knob (never changes a result bit)."""
         _check(self.lib.spmk_csr_set_tuning(self._h, key.encode(), int(value)))
+
+    def spmm_path(self, kid: KernelId, n: int, cfg: Optional[KernelConfig] = None) -> str:
+        """'sell' when spmm(kid, X of width n) runs the lane-per-job seq-ws sweep
+        (+ fold pass; empty rows written by the sweep), else 'tile'."""
+        c = (cfg or KernelConfig())._c()
+        out = C.c_int()
+        _check(self.lib.spmk_spmm_path(self._h, kid.index, C.byref(c), int(n), C.byref(out)))
+        return "sell" if out.value == 1 else "tile"
 
     def get_tuning(self, key: str) -> int:
         v = i64()
