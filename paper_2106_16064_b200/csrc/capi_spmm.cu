@@ -147,9 +147,14 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // overlap the gather-bound sweep; capturable into CUDA graphs).
   // Row-split variants: hub rows (>= L nonzeros) run in hub_kernels.cuh on
   // the side stream, concurrently with the main kernel (disjoint rows of Y).
-  // seq-ws at N % 32 == 0: the lane-per-job sweep writes the empty rows itself
-  const bool sell = id == SPMK_SEQ_BALANCED && sell_eligible(h, (long long)cfg.seq_chunk, N, aligned);
+  // seq-ws / seq-rs at N = 32: the lane-per-job sweep (it writes the empty
+  // rows itself); seq-rs rows of >= L nonzeros go to the hub kernels
+  const bool sell_ws = id == SPMK_SEQ_BALANCED && sell_eligible(h, (long long)cfg.seq_chunk, N, aligned);
+  const bool sell_rs = id == SPMK_SEQ_ROWSPLIT && sell_eligible(h, 1, N, aligned);
+  const bool sell = sell_ws || sell_rs;
   const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
+  // (seq-rs hub threshold 1024 either way: measured on B200 for the sweep, R-MAT
+  // s22 heavy N=32 1343 us vs 1443 at 512 and 1843 at 256, s20 equal)
   const int L = rs ? hub_threshold(h, id) : 0;
   const Plan* hub = L > 0 ? &get_hub_plan(h, L, s) : nullptr;
   const bool hubs = hub && hub->nlong > 0;
@@ -179,7 +184,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.mne = h->mne;
     a.nnz = (int)h->nnz;
     a.N = N;
-    if (id == SPMK_SEQ_ROWSPLIT) {
+    if (sell_rs) {
+      SellPlan& sp = get_sell_plan(h, kSellNoChunk, L > 0 ? L : INT32_MAX, s);
+      timing_record(1, s);
+      launch_sell(h, sp, d_x, N, d_y, nullptr, s);
+      timing_record(2, s);
+    } else if (id == SPMK_SEQ_ROWSPLIT) {
       const long long TS = h->tune.seq_tile_nnz > 0 ? h->tune.seq_tile_nnz : rs_tile_nnz(h->nnz, N);
       Plan& p = get_rs_desc(h, TS, L, hubs ? hub : nullptr, s);
       a.nunits = (int)p.ntiles;
@@ -187,8 +197,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       timing_record(1, s);
       launch_seq(a, false, aligned, s);
       timing_record(2, s);
-    } else if (sell) {
-      SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, s);
+    } else if (sell_ws) {
+      SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, INT32_MAX, s);
       float* H = sp.nslots > 0 ? h->scratch.get((size_t)sp.nslots * N) : nullptr;
       timing_record(1, s);
       launch_sell(h, sp, d_x, N, d_y, H, s);
@@ -438,8 +448,9 @@ spmk_status spmk_spmm_path(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_co
                            int* path) {
   if (!a || !path) return fail(SPMK_EINVAL, "null argument");
   const spmk_kernel_config c = cfg_or_default(cfg);
-  *path = (id == SPMK_SEQ_BALANCED && n > 0 && n <= INT32_MAX &&
-           spmk_host::sell_eligible(a, (long long)c.seq_chunk, (int)n, true))
+  const bool ok = n > 0 && n <= INT32_MAX;
+  *path = ok && ((id == SPMK_SEQ_BALANCED && spmk_host::sell_eligible(a, (long long)c.seq_chunk, (int)n, true)) ||
+                 (id == SPMK_SEQ_ROWSPLIT && spmk_host::sell_eligible(a, 1, (int)n, true)))
               ? 1
               : 0;
   return SPMK_OK;

@@ -176,7 +176,7 @@ struct spmk_csr_s {
   // caches
   std::map<std::tuple<int, long long, long long, long long>, spmk_host::Plan> plans;
   spmk_host::GrowBuffer scratch;   // long-row partial slots (H, T)
-  std::map<std::pair<long long, int>, spmk_host::SellPlan> sell_plans;  // (seq_chunk, shape)
+  std::map<std::tuple<long long, int, int>, spmk_host::SellPlan> sell_plans;  // (seq_chunk, shape, row cap)
   std::map<std::pair<int, int>, spmk_host::HubLayout> hub_layouts;  // (L, N)
   spmk_host::GrowBuffer hub_prod;  // par-rs two-pass hub products
   // host-operand staging: kStageSlots rotating (X, Y) device buffer pairs;
@@ -232,7 +232,9 @@ void launch_seq(const SeqLaunch& a, bool ws, bool aligned, cudaStream_t s);
 
 // ---- launch_sell.cu
 bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned);
-SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s);
+// CH = kSellNoChunk: seq-rs (one job per row); rows of >= lmax nonzeros excluded (hub rows)
+constexpr long long kSellNoChunk = 1LL << 40;
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s);
 void free_sell_plan(SellPlan& p);
 void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s);
 

@@ -133,9 +133,10 @@ bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned) {
          h->nnz < INT32_MAX && h->m < INT32_MAX;
 }
 
-SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s) {
   const int shape = sell_shape_of(h);
-  auto it = h->sell_plans.find({CH, shape});
+  const auto key = std::make_tuple(CH, shape, lmax);
+  auto it = h->sell_plans.find(key);
   if (it != h->sell_plans.end()) return it->second;
   const int mne = h->mne;
   SellPlan p;
@@ -147,7 +148,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
   CK(cudaMemsetAsync(njob.p + mne, 0, sizeof(int), s));
   CK(cudaMemsetAsync(nslot.p + mne, 0, sizeof(int), s));
   CK(cudaMemsetAsync(nmulti.p + mne, 0, sizeof(int), s));
-  sell_count_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, mne, CH, njob.p, nslot.p, nmulti.p); LAUNCHED(1);
+  sell_count_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, mne, CH, lmax, njob.p, nslot.p, nmulti.p); LAUNCHED(1);
   exclusive_scan(njob.p, joff.p, mne + 1, s);
   exclusive_scan(nslot.p, soff.p, mne + 1, s);
   exclusive_scan(nmulti.p, moff.p, mne + 1, s);
@@ -162,7 +163,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
   p.nfold = tot[2];
   DevTmp<int> jstart(J), jlen(J), jout(J);
   if (p.nfold > 0) p.fold = dev_alloc<int4>(p.nfold);
-  sell_jobs_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, h->rid, mne, CH, joff.p, soff.p, moff.p, jstart.p,
+  sell_jobs_kernel<<<grid_for(mne), 256, 0, s>>>(h->crp, h->rid, mne, CH, lmax, joff.p, soff.p, moff.p, jstart.p,
                                                  jlen.p, jout.p, p.fold); LAUNCHED(1);
   if (p.nfold > 1) {  // fold rows with the most slots first (the jobs address H slots, not fold rows)
     DevTmp<int> key(p.nfold), key_s(p.nfold), fidx(p.nfold), fidx_s(p.nfold);
@@ -237,7 +238,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, cudaStream_t s) {
                                                                  h->col, h->val, p.steps); LAUNCHED(1);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));  // temporaries (and cs) are freed on return
-  return h->sell_plans.emplace(std::make_pair(CH, shape), p).first->second;
+  return h->sell_plans.emplace(key, p).first->second;
 }
 
 void free_sell_plan(SellPlan& p) {

@@ -56,11 +56,17 @@ constexpr int kSellStepInts = 64;  // one step: 32 columns + 32 values
 
 // ---------------------------------------------------------------- plan
 // Per compact row: jobs (= segments), H slots and fold flag (rows of >= 2
-// segments).
-__global__ void sell_count_kernel(const int* __restrict__ crp, int mne, long long CH, int* __restrict__ njob,
-                                  int* __restrict__ nslot, int* __restrict__ nmulti) {
+// segments).  seq-rs (spmm_seq_rowsplit, kernels.hpp:339-376) is the same
+// sweep with no chunk cuts (CH beyond any row): one job per row, rows of
+// >= lmax nonzeros left to the hub kernels.
+__global__ void sell_count_kernel(const int* __restrict__ crp, int mne, long long CH, int lmax,
+                                  int* __restrict__ njob, int* __restrict__ nslot, int* __restrict__ nmulti) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mne; i += gridDim.x * blockDim.x) {
     const long long s = crp[i], e = crp[i + 1];
+    if (e - s >= lmax) {  // seq-rs hub row: computed by the hub kernel
+      njob[i] = nslot[i] = nmulti[i] = 0;
+      continue;
+    }
     const int nseg = (int)((e - 1) / CH - s / CH + 1);
     const bool split = nseg > 1;
     njob[i] = split ? nseg : 1;
@@ -72,11 +78,12 @@ __global__ void sell_count_kernel(const int* __restrict__ crp, int mne, long lon
 // Jobs of every compact row (offsets from exclusive scans of the counts) and
 // the fold list {row, first slot, slots, 0} of the split rows.
 __global__ void sell_jobs_kernel(const int* __restrict__ crp, const int* __restrict__ rid, int mne, long long CH,
-                                 const int* __restrict__ joff, const int* __restrict__ soff,
+                                 int lmax, const int* __restrict__ joff, const int* __restrict__ soff,
                                  const int* __restrict__ moff, int* __restrict__ jstart, int* __restrict__ jlen,
                                  int* __restrict__ jout, int4* __restrict__ fold) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mne; i += gridDim.x * blockDim.x) {
     const long long s = crp[i], e = crp[i + 1];
+    if (e - s >= lmax) continue;
     const long long q0 = s / CH;
     const long long nseg = (e - 1) / CH - q0 + 1;
     const int j = joff[i];

@@ -76,7 +76,9 @@ def test_path_selection(mixed):
     assert d.spmm_path(spmk.kSeqBalanced, 64) == "tile"  # N = 32 only by default (measured)
     assert d.spmm_path(spmk.kSeqBalanced, 33) == "tile"
     assert d.spmm_path(spmk.kSeqBalanced, 32, spmk.KernelConfig(seq_chunk=1000)) == "tile"
-    for kid in (spmk.kParRowSplit, spmk.kParBalanced, spmk.kSeqRowSplit):
+    assert d.spmm_path(spmk.kSeqRowSplit, 32) == "sell"
+    assert d.spmm_path(spmk.kSeqRowSplit, 16) == "tile"
+    for kid in (spmk.kParRowSplit, spmk.kParBalanced):
         assert d.spmm_path(kid, 32) == "tile"
     d.set_tuning("seq_impl", 3)
     assert d.spmm_path(spmk.kSeqBalanced, 64) == "sell"
@@ -173,3 +175,19 @@ def test_degenerate_matrices(orc):
             x = orc.make_dense(a.num_cols, 32, chunk)
             y = run(d, x, spmk.KernelConfig(seq_chunk=chunk), seq_impl=2)
             same_bits(y, orc.spmm(csr_of(a), 3, x, seq_chunk=chunk))
+
+
+@pytest.mark.parametrize("hub", [-1, 0, 8, 300])
+def test_seq_rowsplit_through_the_sweep(orc, mixed, hub):
+    """seq-rs (kernels.hpp:339-376) at N = 32: one job per row, rows of >=
+    hub_nnz nonzeros on the hub kernel (-1: default 1024, 0: none)."""
+    a, d = mixed
+    x = orc.make_dense(a.num_cols, 32, 101)
+    for k, v in (("seq_impl", 2), ("hub_nnz", hub)):
+        d.set_tuning(k, v)
+    xd = torch.from_numpy(x).cuda()
+    y = torch.full((a.num_rows, 32), float("nan"), device="cuda")
+    d.spmm(spmk.kSeqRowSplit, xd, y)
+    torch.cuda.synchronize()
+    d.set_tuning("hub_nnz", -1)
+    same_bits(y.cpu().numpy(), orc.spmm(csr_of(a), 2, x))

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--variants", default="seq_impl=1;seq_impl=2")
     ap.add_argument("--lib", default=None)
+    ap.add_argument("--kernel", default="seq-ws")
     args = ap.parse_args()
     if args.lib:
         spmk.spmk.load_library(args.lib)
@@ -45,6 +46,7 @@ def main():
     torch.cuda.synchronize()
     print(f"s{args.scale} e{args.ef} {args.skew}: nnz={d.nnz} maxrow={d.max_row_nnz}", flush=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    kid = spmk.parse_kernel(args.kernel)
     variants = [dict(kv.split("=") for kv in v.split(",")) for v in args.variants.split(";")]
     keys = sorted({k for v in variants for k in v})
     defaults = {k: d.get_tuning(k) for k in keys}
@@ -59,10 +61,10 @@ def main():
                     d.set_tuning(k, int(v.get(k, defaults[k])))
                 y = torch.full((d.num_rows, n), float("nan"), device="cuda")
                 t0 = time.time()
-                d.spmm(spmk.kSeqBalanced, x, y, cfg=cfg)
+                d.spmm(kid, x, y, cfg=cfg)
                 torch.cuda.synchronize()
                 first = time.time() - t0
-                t = timeit(lambda: d.spmm(spmk.kSeqBalanced, x, y, cfg=cfg), flush, args.reps)
+                t = timeit(lambda: d.spmm(kid, x, y, cfg=cfg), flush, args.reps)
                 if ref is None:
                     ref, t_ref = y, t
                 ndiff = int((ref.view(torch.int32) != y.view(torch.int32)).sum().item())
