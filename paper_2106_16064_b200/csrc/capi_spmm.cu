@@ -149,13 +149,16 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // the side stream, concurrently with the main kernel (disjoint rows of Y).
   // seq-ws / seq-rs at N = 32: the lane-per-job sweep (it writes the empty
   // rows itself); seq-rs rows of >= L nonzeros go to the hub kernels
-  const bool sell_ws = id == SPMK_SEQ_BALANCED && sell_eligible(h, (long long)cfg.seq_chunk, N, aligned);
-  const bool sell_rs = id == SPMK_SEQ_ROWSPLIT && sell_eligible(h, 1, N, aligned);
+  const int cw_ws = id == SPMK_SEQ_BALANCED ? sell_width(h, (long long)cfg.seq_chunk, N, aligned) : 0;
+  const int cw_rs = id == SPMK_SEQ_ROWSPLIT ? sell_width(h, 1, N, aligned) : 0;
+  const bool sell_ws = cw_ws > 0, sell_rs = cw_rs > 0;
   const bool sell = sell_ws || sell_rs;
   const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
-  // (seq-rs hub threshold 1024 either way: measured on B200 for the sweep, R-MAT
-  // s22 heavy N=32 1343 us vs 1443 at 512 and 1843 at 256, s20 equal)
-  const int L = rs ? hub_threshold(h, id) : 0;
+  // seq-rs hub threshold under the sweep (measured on B200, R-MAT heavy):
+  // N = 32 1024 (s22: 1343 us vs 1443 at 512, 1843 at 256; s20 equal);
+  // N = 8 / 16 (4 / 2 jobs per lane: longer slices) 512 (N=8 s20 282 vs 402
+  // us at 1024, s22 equal; N=16 s20 309 vs 367, s22 1107 vs 974)
+  const int L = rs ? ((cw_rs > 0 && cw_rs < 32 && h->tune.hub_nnz < 0) ? 512 : hub_threshold(h, id)) : 0;
   const Plan* hub = L > 0 ? &get_hub_plan(h, L, s) : nullptr;
   const bool hubs = hub && hub->nlong > 0;
   const bool zero_side = h->nempty > 0 && !sell;
@@ -185,7 +188,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     a.nnz = (int)h->nnz;
     a.N = N;
     if (sell_rs) {
-      SellPlan& sp = get_sell_plan(h, kSellNoChunk, L > 0 ? L : INT32_MAX, s);
+      SellPlan& sp = get_sell_plan(h, kSellNoChunk, L > 0 ? L : INT32_MAX, cw_rs, s);
       timing_record(1, s);
       launch_sell(h, sp, d_x, N, d_y, nullptr, s);
       timing_record(2, s);
@@ -198,7 +201,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_seq(a, false, aligned, s);
       timing_record(2, s);
     } else if (sell_ws) {
-      SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, INT32_MAX, s);
+      SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, INT32_MAX, cw_ws, s);
       float* H = sp.nslots > 0 ? h->scratch.get((size_t)sp.nslots * N) : nullptr;
       timing_record(1, s);
       launch_sell(h, sp, d_x, N, d_y, H, s);
@@ -449,8 +452,8 @@ spmk_status spmk_spmm_path(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_co
   if (!a || !path) return fail(SPMK_EINVAL, "null argument");
   const spmk_kernel_config c = cfg_or_default(cfg);
   const bool ok = n > 0 && n <= INT32_MAX;
-  *path = ok && ((id == SPMK_SEQ_BALANCED && spmk_host::sell_eligible(a, (long long)c.seq_chunk, (int)n, true)) ||
-                 (id == SPMK_SEQ_ROWSPLIT && spmk_host::sell_eligible(a, 1, (int)n, true)))
+  *path = ok && ((id == SPMK_SEQ_BALANCED && spmk_host::sell_width(a, (long long)c.seq_chunk, (int)n, true) > 0) ||
+                 (id == SPMK_SEQ_ROWSPLIT && spmk_host::sell_width(a, 1, (int)n, true) > 0))
               ? 1
               : 0;
   return SPMK_OK;

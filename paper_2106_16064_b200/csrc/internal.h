@@ -100,6 +100,7 @@ constexpr long long kSellMaxChunk = 512;
 struct SellPlan {
   long long CH = 0;
   int shape = 0;            // sweep shape (launch_sell.cu kSellShapes)
+  int cw = 32;              // column width (8 / 16 / 32: 4 / 2 / 1 jobs per lane)
   int* steps = nullptr;     // nsteps x 64 ints
   long long nsteps = 0;
   int* cstep = nullptr;     // nchunks + 1 work-queue chunk starts (step indices)
@@ -231,10 +232,11 @@ struct SeqLaunch {
 void launch_seq(const SeqLaunch& a, bool ws, bool aligned, cudaStream_t s);
 
 // ---- launch_sell.cu
-bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned);
+// column width of the lane-per-job sweep for (seq_chunk, N), 0 = not eligible
+int sell_width(const spmk_csr_s* h, long long CH, int N, bool aligned);
 // CH = kSellNoChunk: seq-rs (one job per row); rows of >= lmax nonzeros excluded (hub rows)
 constexpr long long kSellNoChunk = 1LL << 40;
-SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s);
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStream_t s);
 void free_sell_plan(SellPlan& p);
 void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s);
 

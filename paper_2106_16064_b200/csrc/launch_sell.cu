@@ -26,22 +26,39 @@ struct SellShape {
   void (*launch)(dim3, const SellArgs&, cudaStream_t);
   int wpc, smem;
 };
-template <int S, int C, int WPC, int MINB>
+template <int CW, int S, int C, int WPC, int MINB>
 void sell_launch_t(dim3 grid, const SellArgs& a, cudaStream_t s) {
-  seq_sell_kernel<S, C, WPC, MINB><<<grid, WPC * 32, sell_smem_bytes<S, C, WPC>(), s>>>(a);
+  seq_sell_kernel<CW, S, C, WPC, MINB><<<grid, WPC * 32, sell_smem_bytes<CW, S, C, WPC>(), s>>>(a);
 }
-template <int S, int C, int WPC, int MINB>
+template <int CW, int S, int C, int WPC, int MINB>
 constexpr SellShape sell_shape() {
-  return SellShape{reinterpret_cast<const void*>(seq_sell_kernel<S, C, WPC, MINB>), sell_launch_t<S, C, WPC, MINB>,
-                   WPC, sell_smem_bytes<S, C, WPC>()};
+  return SellShape{reinterpret_cast<const void*>(seq_sell_kernel<CW, S, C, WPC, MINB>),
+                   sell_launch_t<CW, S, C, WPC, MINB>, WPC, sell_smem_bytes<CW, S, C, WPC>()};
 }
-const SellShape kSellShapes[] = {
-    sell_shape<4, 8, 4, 3>(),   // 0: 12 warps / SM, 3 steps of rows in flight per warp
-    sell_shape<2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
-    sell_shape<4, 8, 12, 1>(),  // 2: 12 warps in one CTA
-    sell_shape<8, 16, 3, 2>(),  // 3: 6 warps, 7 in flight
+// [column width 32 / 16 / 8][sell_cfg]; a step's rows are 4 KB at every width,
+// its A part 256 B x (32 / CW)
+constexpr int kSellShapeCount = 4;
+const SellShape kSellShapes[3][kSellShapeCount] = {
+    {
+        sell_shape<32, 4, 8, 4, 3>(),   // 0: 12 warps / SM, 3 steps of rows in flight per warp
+        sell_shape<32, 2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
+        sell_shape<32, 4, 8, 12, 1>(),  // 2: 12 warps in one CTA
+        sell_shape<32, 8, 16, 3, 2>(),  // 3: 6 warps, 7 in flight
+    },
+    {
+        sell_shape<16, 4, 8, 5, 2>(),   // 0: 10 warps / SM
+        sell_shape<16, 2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
+        sell_shape<16, 4, 8, 4, 2>(),   // 2: 8 warps
+        sell_shape<16, 4, 8, 3, 3>(),   // 3: 9 warps
+    },
+    {
+        sell_shape<8, 4, 8, 3, 3>(),    // 0: 9 warps / SM
+        sell_shape<8, 2, 4, 8, 2>(),    // 1: 16 warps, 1 in flight
+        sell_shape<8, 4, 8, 4, 2>(),    // 2: 8 warps
+        sell_shape<8, 2, 4, 6, 3>(),    // 3: 18 warps, 1 in flight
+    },
 };
-constexpr int kSellShapeCount = sizeof(kSellShapes) / sizeof(kSellShapes[0]);
+int cw_index(int cw) { return cw == 32 ? 0 : (cw == 16 ? 1 : 2); }
 
 template <typename T>
 struct DevTmp {
@@ -74,20 +91,20 @@ __global__ void iota_kernel(int* p, int n) {
 }
 
 // Resident CTAs per SM of a sweep shape (and its shared-memory opt-in), per device.
-int sell_blocks_per_sm(int shape) {
+int sell_blocks_per_sm(int cw, int shape) {
   static std::mutex mu;
-  static std::map<std::pair<int, int>, int> cache;
+  static std::map<std::tuple<int, int, int>, int> cache;
   int dev = 0;
   CK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find({dev, shape});
+  auto it = cache.find({dev, cw, shape});
   if (it != cache.end()) return it->second;
-  const SellShape& sh = kSellShapes[shape];
+  const SellShape& sh = kSellShapes[cw_index(cw)][shape];
   int bps = 1;
   CK(cudaFuncSetAttribute(sh.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sh.smem));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sh.fn, sh.wpc * 32, sh.smem));
   if (bps < 1) bps = 1;
-  cache[{dev, shape}] = bps;
+  cache[{dev, cw, shape}] = bps;
   return bps;
 }
 
@@ -123,25 +140,32 @@ extern "C" int spmk_sell_trace(unsigned long long* out, int cap) {
   return n;
 }
 
-bool sell_eligible(const spmk_csr_s* h, long long CH, int N, bool aligned) {
-  // N = 32 only: at N = 64 / 128 the tile sweep (16 / 32 lanes per unit,
-  // 256 / 512-byte rows per gather) measured 7 % / 34 % faster on B200
-  const bool shape_ok =
-      h->tune.seq_impl == 2 ? N == 32 : (h->tune.seq_impl == 3 && N % 32 == 0 && N / 32 <= kSellMaxTiles);
-  return shape_ok && aligned && CH <= kSellMaxChunk && h->k < INT32_MAX &&
-         (unsigned long long)h->k * (unsigned long long)(N / 4) < (1ull << 32) &&
-         h->nnz < INT32_MAX && h->m < INT32_MAX;
+int sell_width(const spmk_csr_s* h, long long CH, int N, bool aligned) {
+  // N = 8 / 16 / 32 (one tile of 8 / 16 / 32 columns, 4 / 2 / 1 jobs per
+  // lane); at N = 64 / 128 the tile sweep (16 / 32 lanes per unit, 256 /
+  // 512-byte rows per gather) measured 7 % / 34 % faster on B200, so 32-column
+  // tiles of wider X only with seq_impl 3
+  if (h->tune.seq_impl < 2) return 0;
+  int cw = 0;
+  if (N == 32 || N == 16 || N == 8) cw = N;
+  else if (h->tune.seq_impl == 3 && N % 32 == 0 && N / 32 <= kSellMaxTiles) cw = 32;
+  const bool ok = cw > 0 && aligned && CH <= kSellMaxChunk && h->k < INT32_MAX &&
+                  (unsigned long long)h->k * (unsigned long long)(N / 4) < (1ull << 32) && h->nnz < INT32_MAX &&
+                  h->m < INT32_MAX;
+  return ok ? cw : 0;
 }
 
-SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s) {
+SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStream_t s) {
   const int shape = sell_shape_of(h);
-  const auto key = std::make_tuple(CH, shape, lmax);
+  const auto key = std::make_tuple(CH, shape * 64 + cw, lmax);
+  const int jps = 32 * (32 / cw);  // jobs per slice
   auto it = h->sell_plans.find(key);
   if (it != h->sell_plans.end()) return it->second;
   const int mne = h->mne;
   SellPlan p;
   p.CH = CH;
   p.shape = shape;
+  p.cw = cw;
   // jobs per compact row, H slots, fold rows
   DevTmp<int> njob(mne + 1), nslot(mne + 1), nmulti(mne + 1);
   DevTmp<int> joff(mne + 1), soff(mne + 1), moff(mne + 1);
@@ -197,10 +221,10 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s) {
     DevTmp<unsigned char> tmp(bytes);
     CK(cub::DeviceRadixSort::SortPairsDescending(tmp.p, bytes, jlen.p, slen.p, idx.p, sidx.p, J, 0, 16, s));
   }
-  const int nsl = (J + 31) / 32;
+  const int nsl = (int)(((long long)J + jps - 1) / jps);
   DevTmp<long long> lsteps(nsl + 1), lcost(nsl + 1), step_ex(nsl + 1);
   CK(cudaMemsetAsync(lsteps.p + nsl, 0, sizeof(long long), s));
-  sell_slice_kernel<<<grid_for(nsl), 256, 0, s>>>(slen.p, nsl, lsteps.p, lcost.p); LAUNCHED(1);
+  sell_slice_kernel<<<grid_for(nsl), 256, 0, s>>>(slen.p, nsl, jps, lsteps.p, lcost.p); LAUNCHED(1);
   exclusive_scan(lsteps.p, step_ex.p, nsl + 1, s);
   std::vector<long long> sx((size_t)nsl + 1);
   CK(cudaMemcpyAsync(sx.data(), step_ex.p, sizeof(long long) * sx.size(), cudaMemcpyDeviceToHost, s));
@@ -208,12 +232,12 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s) {
   const long long T = sx[(size_t)nsl];
   if (T >= INT32_MAX) throw CudaError{SPMK_EUNSUPPORTED, "sell layout: too many steps"};
   p.nsteps = T;
-  p.steps = dev_alloc<int>((size_t)T * kSellStepInts);
+  p.steps = dev_alloc<int>((size_t)T * 2 * jps);
   int dev = 0, sms = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  p.blocks = sms * sell_blocks_per_sm(shape);
-  p.nwarps = p.blocks * kSellShapes[shape].wpc;
+  p.blocks = sms * sell_blocks_per_sm(cw, shape);
+  p.nwarps = p.blocks * kSellShapes[cw_index(cw)][shape].wpc;
   // Chunks of whole slices for the warps' work queue, guided sizes: about
   // remaining / (4 W) steps, clamped to [kSellChunkMin, kSellChunkMax] (a
   // slice longer than that is one chunk); the first W are the warps' first
@@ -234,7 +258,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, cudaStream_t s) {
   CK(cudaMemcpyAsync(p.cstep, cs.data(), sizeof(int) * cs.size(), cudaMemcpyHostToDevice, s));
   p.sched = dev_alloc<int>(2 * kSellMaxTiles);
   CK(cudaMemsetAsync(p.sched, 0, sizeof(int) * 2 * kSellMaxTiles, s));
-  sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, step_ex.p, jstart.p, jout.p,
+  sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, jps, step_ex.p, jstart.p, jout.p,
                                                                  h->col, h->val, p.steps); LAUNCHED(1);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));  // temporaries (and cs) are freed on return
@@ -250,7 +274,7 @@ void free_sell_plan(SellPlan& p) {
 }
 
 void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s) {
-  const int tiles = N / 32;
+  const int tiles = N / p.cw;
   SellArgs a{};
   a.steps = p.steps;
   a.cstep = p.cstep;
@@ -262,8 +286,8 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
   a.N = N;
   a.one2 = kOnePair;
   a.trace = sell_trace_buffer(p.nwarps);
-  sell_blocks_per_sm(p.shape);  // shared-memory opt-in on this device
-  kSellShapes[p.shape].launch(dim3(p.blocks, tiles), a, s); LAUNCHED(1);
+  sell_blocks_per_sm(p.cw, p.shape);  // shared-memory opt-in on this device
+  kSellShapes[cw_index(p.cw)][p.shape].launch(dim3(p.blocks, tiles), a, s); LAUNCHED(1);
   if (p.nfold > 0) {
     // programmatic dependent launch: scheduled while the sweep drains
     cudaLaunchConfig_t lc = {};

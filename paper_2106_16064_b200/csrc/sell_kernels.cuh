@@ -52,7 +52,9 @@
 
 namespace spmk_dev {
 
-constexpr int kSellStepInts = 64;  // one step: 32 columns + 32 values
+// One step of a slice of 32 G jobs (G = 32 / CW jobs per lane, CW = the
+// sweep's column width): 32 G columns + 32 G values.
+__host__ __device__ constexpr int sell_step_ints(int cw) { return 2 * 32 * (32 / cw); }
 
 // ---------------------------------------------------------------- plan
 // Per compact row: jobs (= segments), H slots and fold flag (rows of >= 2
@@ -118,37 +120,40 @@ __global__ void sell_empty_jobs_kernel(const int* __restrict__ erow, int nempty,
 // Slice lengths (jobs sorted by length, descending: the slice's first job is
 // its longest) -> steps (1 + L) and balancing cost (steps + 1: the header and
 // the epilogue cost about one more step).
-__global__ void sell_slice_kernel(const int* __restrict__ slen_sorted, int nsl, long long* __restrict__ steps,
-                                  long long* __restrict__ cost) {
+__global__ void sell_slice_kernel(const int* __restrict__ slen_sorted, int nsl, int jps,
+                                  long long* __restrict__ steps, long long* __restrict__ cost) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x) {
-    const int L = slen_sorted[32 * s];
+    const int L = slen_sorted[(long long)jps * s];
     steps[s] = 1 + L;
     cost[s] = 2 + L;
   }
 }
 
-// One warp per slice: header + data steps.
-__global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __restrict__ slen, int J, int nsl,
+// One warp per slice (jps = 32 G jobs: position g * 32 + lane): header + data
+// steps of 2 jps ints.
+__global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __restrict__ slen, int J, int nsl, int jps,
                                  const long long* __restrict__ step_ex, const int* __restrict__ jstart,
                                  const int* __restrict__ jout,
                                  const int* __restrict__ col, const float* __restrict__ val, int* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   for (long long s = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; s < nsl;
        s += ((long long)gridDim.x * blockDim.x) >> 5) {
-    const long long j = 32 * s + lane;
-    const bool ok = j < J;
-    const int L = slen[32 * s];
-    const int idx = ok ? sidx[j] : 0;
-    const int len = ok ? slen[j] : 0;
-    const int st = ok ? jstart[idx] : 0;
-    int* p = out + step_ex[s] * kSellStepInts;
-    p[lane] = ok ? jout[idx] : -1;
-    p[32 + lane] = len;
-    for (int t = 0; t < L; ++t) {
-      int* q = p + (long long)(t + 1) * kSellStepInts;
-      const bool in = t < len;
-      q[lane] = in ? col[st + t] : 0;
-      q[32 + lane] = in ? __float_as_int(val[st + t]) : 0;
+    const int L = slen[(long long)jps * s];
+    int* p = out + step_ex[s] * 2 * jps;
+    for (int pos = lane; pos < jps; pos += 32) {
+      const long long j = (long long)jps * s + pos;
+      const bool ok = j < J;
+      const int idx = ok ? sidx[j] : 0;
+      const int len = ok ? slen[j] : 0;
+      const int st = ok ? jstart[idx] : 0;
+      p[pos] = ok ? jout[idx] : -1;
+      p[jps + pos] = len;
+      for (int t = 0; t < L; ++t) {
+        int* q = p + (long long)(t + 1) * 2 * jps;
+        const bool in = t < len;
+        q[pos] = in ? col[st + t] : 0;
+        q[jps + pos] = in ? __float_as_int(val[st + t]) : 0;
+      }
     }
   }
 }
@@ -188,20 +193,27 @@ struct SellArgs {
   unsigned long long* trace;      // dev: per-warp {start, end, steps, slices} (%globaltimer), or null
 };
 
-constexpr int kSellStage = 32 * 128;  // one step's 32 dense rows in the ring
-template <int S, int C>
+constexpr int kSellStage = 4096;  // one step's 32 G dense rows of CW floats in the ring
+template <int CW, int S, int C>
 __host__ __device__ constexpr int sell_warp_bytes() {
-  return S * kSellStage + C * kSellStepInts * 4;
+  return S * kSellStage + C * sell_step_ints(CW) * 4;
 }
-template <int S, int C, int WPC>
+template <int CW, int S, int C, int WPC>
 __host__ __device__ constexpr int sell_smem_bytes() {
-  return WPC * sell_warp_bytes<S, C>();
+  return WPC * sell_warp_bytes<CW, S, C>();
 }
 
-template <int S, int C, int WPC, int MINB>
+template <int CW, int S, int C, int WPC, int MINB>
 __global__ void __launch_bounds__(WPC * 32, MINB)
 seq_sell_kernel(const SellArgs a) {
+  static_assert(CW == 8 || CW == 16 || CW == 32, "column width");
   static_assert(S >= 2 && C >= 2 * S - 1 && (S & (S - 1)) == 0 && (C & (C - 1)) == 0, "ring depths");
+  constexpr int G = 32 / CW;           // jobs per lane
+  constexpr int JPS = 32 * G;          // jobs per slice = dense rows per step
+  constexpr int SI = 2 * JPS;          // ints per step
+  constexpr int RB = 4 * CW;           // bytes per dense row
+  constexpr int CPR = CW / 4;          // 16-byte chunks per row
+  constexpr int LPR = CW / 4;          // LDGSTS lanes per row
   extern __shared__ __align__(128) unsigned char s_sell[];
   // the fold pass (a programmatic dependent) may be scheduled as CTAs drain;
   // it still waits for this grid's completion before reading H
@@ -214,18 +226,19 @@ seq_sell_kernel(const SellArgs a) {
   int nsteps = 0, nslices = 0;
   if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-  unsigned char* wb = s_sell + warp * sell_warp_bytes<S, C>();
-  const int* cr = reinterpret_cast<const int*>(wb + S * kSellStage);  // [C][64]
+  unsigned char* wb = s_sell + warp * sell_warp_bytes<CW, S, C>();
+  const int* cr = reinterpret_cast<const int*>(wb + S * kSellStage);  // [C][SI]
   const unsigned xr0 = smem_addr(wb);
   const unsigned cr0 = xr0 + S * kSellStage;
-  const int col0 = blockIdx.y * 32;
+  const int col0 = blockIdx.y * CW;
   const int* steps = a.steps;
-  // LDGSTS lanes: rows 8 * (lane >> 3) + i (i = 0..7), 16-byte chunk lane & 7
-  const int rg = lane >> 3, ch = lane & 7;
+  // LDGSTS lanes: group q = lane / LPR copies rows 8 q + i (i = 0..7), 16-byte
+  // chunk lane % LPR: every instruction moves 512 contiguous-per-row bytes
+  const int q = lane / LPR, ch = lane % LPR;
   // 32-bit row offsets in 16-byte units (the plan checks K * N / 4 < 2^32)
   const float4* xg = reinterpret_cast<const float4*>(a.X + col0);
   const unsigned n16 = (unsigned)a.N / 4;
-  const unsigned xdst0 = xr0 + (unsigned)(rg * 8 * 128 + ch * 16);
+  const unsigned xdst0 = xr0 + (unsigned)(q * 8 * RB + ch * 16);
 
   // Work: chunks of whole slices (plan: a.cstep), heaviest first.  Warp w
   // starts with chunk w and claims the next one (atomic counter) as soon as
@@ -264,25 +277,27 @@ seq_sell_kernel(const SellArgs a) {
     blen = 0;
   }
 
-  // step g into step-ring slot cs: lanes 0..15, 16 B each
+  // step g into step-ring slot cs: SI / 4 lanes' worth of 16-byte copies
   auto fetch_step = [&](int g, int cs) {
-    if (lane < 16 && g >= 0) cp16(cr0 + cs * 256 + lane * 16, steps + (size_t)g * kSellStepInts + lane * 4);
+    if (g < 0) return;
+#pragma unroll
+    for (int o = lane; o < SI / 4; o += 32) cp16(cr0 + (cs * SI + o * 4) * 4, steps + (size_t)g * SI + o * 4);
   };
   int prem = 0;  // producer: data steps left in the current slice
-  // dense rows of step p (step slot pcs) into row-ring slot pxs
+  // dense rows of step p (step slot pcs) into row-ring slot pxs (prologue)
   auto produce = [&](int p, int pcs, int pxs) {
     if (p < 0) return;
     if (prem == 0) {  // header: no rows
-      prem = cr[pcs * kSellStepInts + 32];
+      prem = cr[pcs * SI + JPS];
       return;
     }
     --prem;
-    const int4 c0 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg];
-    const int4 c1 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg + 1];
+    const int4 c0 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q];
+    const int4 c1 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q + 1];
     const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     const unsigned d = xdst0 + pxs * kSellStage;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cp16(d + i * 128, xg + ((unsigned)cc[i] * n16 + ch));
+    for (int i = 0; i < 8; ++i) cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
   };
 
   // prologue: steps 0 .. C-2 (one group each), then rows of steps 0 .. S-2
@@ -299,24 +314,39 @@ seq_sell_kernel(const SellArgs a) {
     cp_commit();
   }
 
-  // this lane's row in a ring stage, read in rotated chunk order
-  unsigned roff[8];
+  // This lane's jobs sit at positions g * 32 + lane of a slice; their rows are
+  // read in rotated chunk order (chunk (c + rot) % CPR at slot c) so the 8
+  // lanes of a quarter warp hit 8 different bank groups.
+  constexpr int ROT_SHIFT = CW == 32 ? 0 : (CW == 16 ? 1 : 2);
+  const int rot = (lane >> ROT_SHIFT) & (CPR - 1);
+  unsigned roff[G][CPR];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) roff[c] = (unsigned)(lane * 128 + (((c + lane) & 7) * 16));
-  float acc[32];
+  for (int g = 0; g < G; ++g)
 #pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-  int out = -1, crem = 0;
-  int t = 0, len = 0;  // position in the slice, this lane's job length
+    for (int c = 0; c < CPR; ++c) roff[g][c] = (unsigned)((g * 32 + lane) * RB + (((c + rot) & (CPR - 1)) * 16));
+  float acc[G][CW];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int c = 0; c < CW; ++c) acc[g][c] = 0.f;
+  int out[G], len[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) out[g] = -1, len[g] = 0;
+  int crem = 0, t = 0;  // steps left in the slice, position in it
   const size_t ystride = (size_t)a.N;
   auto epilogue = [&]() {
-    if (out == -1) return;
-    float* base = (out >= 0 ? a.Y + (size_t)out * ystride : a.H + (size_t)(out & 0x7fffffff) * ystride) + col0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int k = (c + lane) & 7;  // slot c holds chunk (c + lane) & 7
-      if (out >= 0) st_y4(base + 4 * k, acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
-      else *reinterpret_cast<float4*>(base + 4 * k) = make_float4(acc[4 * c], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
+    for (int g = 0; g < G; ++g) {
+      if (out[g] == -1) continue;
+      float* base =
+          (out[g] >= 0 ? a.Y + (size_t)out[g] * ystride : a.H + (size_t)(out[g] & 0x7fffffff) * ystride) + col0;
+#pragma unroll
+      for (int c = 0; c < CPR; ++c) {
+        const int k = (c + rot) & (CPR - 1);  // slot c holds chunk (c + rot) % CPR
+        const float* o = &acc[g][4 * c];
+        if (out[g] >= 0) st_y4(base + 4 * k, o[0], o[1], o[2], o[3]);
+        else *reinterpret_cast<float4*>(base + 4 * k) = make_float4(o[0], o[1], o[2], o[3]);
+      }
     }
   };
 
@@ -348,35 +378,41 @@ seq_sell_kernel(const SellArgs a) {
     int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
     if (p >= 0) {
       if (prem == 0) {  // header: no rows
-        prem = cr[pcs * kSellStepInts + 32];
+        prem = cr[pcs * SI + JPS];
       } else {
         --prem;
         issue = true;
-        c0 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg];
-        c1 = reinterpret_cast<const int4*>(cr + pcs * kSellStepInts)[2 * rg + 1];
+        c0 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q];
+        c1 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q + 1];
       }
     }
     const int f = map(k + C - 1);
     // consumer: position k
-    const int* cw = cr + (it & (C - 1)) * kSellStepInts;
+    const int* cw = cr + (it & (C - 1)) * SI;
     if (crem == 0) {  // header: finish the previous slice, start the next
       ++nslices;
       epilogue();
-      out = cw[lane];
-      len = cw[32 + lane];
-      crem = cw[32];  // lane 0 runs the slice's longest job
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        out[g] = cw[g * 32 + lane];
+        len[g] = cw[JPS + g * 32 + lane];
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[g][c] = 0.f;
+      }
+      crem = cw[JPS];  // position 0 holds the slice's longest job
       t = 0;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] = 0.f;
     } else {
-      const float v = __int_as_float(cw[32 + lane]);
       const unsigned char* xrow = wb + (it & (S - 1)) * kSellStage;
-      if (t < len) {  // padding positions add nothing (also when X holds inf / NaN)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 x = *reinterpret_cast<const float4*>(xrow + roff[c]);
-          f2_mac(acc[4 * c], acc[4 * c + 1], v, x.x, x.y, a.one2);
-          f2_mac(acc[4 * c + 2], acc[4 * c + 3], v, x.z, x.w, a.one2);
+      for (int g = 0; g < G; ++g) {
+        const float v = __int_as_float(cw[JPS + g * 32 + lane]);
+        if (t < len[g]) {  // padding positions add nothing (also when X holds inf / NaN)
+#pragma unroll
+          for (int c = 0; c < CPR; ++c) {
+            const float4 x = *reinterpret_cast<const float4*>(xrow + roff[g][c]);
+            f2_mac(acc[g][4 * c], acc[g][4 * c + 1], v, x.x, x.y, a.one2);
+            f2_mac(acc[g][4 * c + 2], acc[g][4 * c + 3], v, x.z, x.w, a.one2);
+          }
         }
       }
       ++t;
@@ -388,7 +424,7 @@ seq_sell_kernel(const SellArgs a) {
       const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       const unsigned d = xdst0 + ((it + S - 1) & (S - 1)) * kSellStage;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cp16(d + i * 128, xg + ((unsigned)cc[i] * n16 + ch));
+      for (int i = 0; i < 8; ++i) cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
     }
     fetch_step(f, (it + C - 1) & (C - 1));
     cp_commit();
@@ -436,7 +472,7 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float
                  float* __restrict__ Y, int N) {
   constexpr int WPB = kFoldThreads / 32;
   __shared__ float buf[kFoldStage][33];
-  const int tiles = N >> 5;
+  const int tiles = N >= 32 ? N >> 5 : 1;  // N < 32 (the 8 / 16-column sweeps): lanes >= N idle
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nbig_items = nbig * tiles;
   if ((int)blockIdx.x < nbig_items) {
@@ -444,7 +480,8 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float
     const int c0 = ((int)blockIdx.x - f * tiles) * 32;
     const int4 d = fold[f];
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const float* h = H + (size_t)d.y * N + c0 + lane;
+    const bool colok = c0 + lane < N;
+    const float* h = H + (size_t)d.y * N + (colok ? c0 + lane : 0);
     float y = 0.f;
     for (int k0 = 0; k0 < d.z; k0 += kFoldStage) {
       const int n = min(kFoldStage, d.z - k0);
@@ -471,7 +508,7 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float
       }
       __syncthreads();
     }
-    if (warp == 0) st_y(Y + (size_t)d.x * N + c0 + lane, y);
+    if (warp == 0 && colok) st_y(Y + (size_t)d.x * N + c0 + lane, y);
     return;
   }
   // kFoldRows consecutive (row, tile) items per warp, all their loads in flight
@@ -483,8 +520,8 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float
   for (int r = 0; r < kFoldRows; ++r) {
     const int it = item0 + r;
     const int f = tiles == 1 ? it : it / tiles;
-    d[r] = it < nitems ? fold[f] : make_int4(0, 0, 0, 0);
     c[r] = (it - f * tiles) * 32 + lane;
+    d[r] = it < nitems && c[r] < N ? fold[f] : make_int4(0, 0, 0, 0);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (item0 >= nitems) return;

@@ -73,11 +73,15 @@ def test_path_selection(mixed):
     a, d = mixed
     d.set_tuning("seq_impl", 2)
     assert d.spmm_path(spmk.kSeqBalanced, 32) == "sell"
-    assert d.spmm_path(spmk.kSeqBalanced, 64) == "tile"  # N = 32 only by default (measured)
+    assert d.spmm_path(spmk.kSeqBalanced, 64) == "tile"  # N = 8 / 16 / 32 by default (measured)
+    assert d.spmm_path(spmk.kSeqBalanced, 16) == "sell"
+    assert d.spmm_path(spmk.kSeqBalanced, 8) == "sell"
+    assert d.spmm_path(spmk.kSeqBalanced, 4) == "tile"
     assert d.spmm_path(spmk.kSeqBalanced, 33) == "tile"
     assert d.spmm_path(spmk.kSeqBalanced, 32, spmk.KernelConfig(seq_chunk=1000)) == "tile"
     assert d.spmm_path(spmk.kSeqRowSplit, 32) == "sell"
-    assert d.spmm_path(spmk.kSeqRowSplit, 16) == "tile"
+    assert d.spmm_path(spmk.kSeqRowSplit, 8) == "sell"
+    assert d.spmm_path(spmk.kSeqRowSplit, 12) == "tile"
     for kid in (spmk.kParRowSplit, spmk.kParBalanced):
         assert d.spmm_path(kid, 32) == "tile"
     d.set_tuning("seq_impl", 3)
@@ -87,10 +91,11 @@ def test_path_selection(mixed):
     d.set_tuning("seq_impl", 2)
 
 
+@pytest.mark.parametrize("n", [8, 16, 32])
 @pytest.mark.parametrize("chunk", [1, 7, 256, 512])
-def test_bit_exact_mixed_rows(orc, mixed, chunk):
+def test_bit_exact_mixed_rows(orc, mixed, chunk, n):
     a, d = mixed
-    x = orc.make_dense(a.num_cols, 32, 77 + chunk)
+    x = orc.make_dense(a.num_cols, n, 77 + chunk)
     cfg = spmk.KernelConfig(seq_chunk=chunk)
     y = run(d, x, cfg, seq_impl=2)
     same_bits(y, orc.spmm(csr_of(a), 3, x, seq_chunk=chunk))
@@ -98,10 +103,11 @@ def test_bit_exact_mixed_rows(orc, mixed, chunk):
     assert np.all(y[empty] == 0) and not np.any(np.signbit(y[empty]))
 
 
+@pytest.mark.parametrize("n", [8, 16, 32])
 @pytest.mark.parametrize("shape", [0, 1, 2, 3])
-def test_every_sweep_shape(orc, mixed, shape):
+def test_every_sweep_shape(orc, mixed, shape, n):
     a, d = mixed
-    x = orc.make_dense(a.num_cols, 32, 91)
+    x = orc.make_dense(a.num_cols, n, 91)
     y = run(d, x, None, seq_impl=2, sell_cfg=shape)
     d.set_tuning("sell_cfg", 0)
     same_bits(y, orc.spmm(csr_of(a), 3, x))
@@ -116,14 +122,15 @@ def test_multi_tile_variant(orc, mixed, n):
     same_bits(y, orc.spmm(csr_of(a), 3, x))
 
 
-def test_padding_lanes_ignore_inf_nan(orc, mixed):
+@pytest.mark.parametrize("n", [8, 16, 32])
+def test_padding_lanes_ignore_inf_nan(orc, mixed, n):
     """Padding positions gather X row 0; with inf / NaN there they must add
     nothing (the reference never touches them)."""
     a, d = mixed
-    x = orc.make_dense(a.num_cols, 32, 5)
-    x[0, :8] = np.inf
-    x[0, 8:16] = -np.inf
-    x[0, 16:] = np.nan
+    x = orc.make_dense(a.num_cols, n, 5)
+    x[0, : n // 4] = np.inf
+    x[0, n // 4: n // 2] = -np.inf
+    x[0, n // 2:] = np.nan
     x[7, 3] = np.nan
     y = run(d, x, None, seq_impl=2)
     same_bits(y, orc.spmm(csr_of(a), 3, x))
@@ -172,21 +179,23 @@ def test_degenerate_matrices(orc):
     for a in cases:
         d = spmk.DeviceCsr.from_host(a)
         for chunk in (1, 3, 256):
-            x = orc.make_dense(a.num_cols, 32, chunk)
-            y = run(d, x, spmk.KernelConfig(seq_chunk=chunk), seq_impl=2)
-            same_bits(y, orc.spmm(csr_of(a), 3, x, seq_chunk=chunk))
+            for n in (8, 16, 32):
+                x = orc.make_dense(a.num_cols, n, chunk)
+                y = run(d, x, spmk.KernelConfig(seq_chunk=chunk), seq_impl=2)
+                same_bits(y, orc.spmm(csr_of(a), 3, x, seq_chunk=chunk))
 
 
+@pytest.mark.parametrize("n", [8, 16, 32])
 @pytest.mark.parametrize("hub", [-1, 0, 8, 300])
-def test_seq_rowsplit_through_the_sweep(orc, mixed, hub):
-    """seq-rs (kernels.hpp:339-376) at N = 32: one job per row, rows of >=
-    hub_nnz nonzeros on the hub kernel (-1: default 1024, 0: none)."""
+def test_seq_rowsplit_through_the_sweep(orc, mixed, hub, n):
+    """seq-rs (kernels.hpp:339-376) at N = 8 / 16 / 32: one job per row, rows
+    of >= hub_nnz nonzeros on the hub kernel (-1: default, 0: none)."""
     a, d = mixed
-    x = orc.make_dense(a.num_cols, 32, 101)
+    x = orc.make_dense(a.num_cols, n, 101)
     for k, v in (("seq_impl", 2), ("hub_nnz", hub)):
         d.set_tuning(k, v)
     xd = torch.from_numpy(x).cuda()
-    y = torch.full((a.num_rows, 32), float("nan"), device="cuda")
+    y = torch.full((a.num_rows, n), float("nan"), device="cuda")
     d.spmm(spmk.kSeqRowSplit, xd, y)
     torch.cuda.synchronize()
     d.set_tuning("hub_nnz", -1)
