@@ -470,7 +470,7 @@ def selection_loss_summary():
     out["cells"] = len(recs["reference"]) // 5
     out["sweep"] = "uniform/banded/heavy x 2^18, 2^20 x N=1..128 (reduced cfg3), median of 3, L2 flushed"
     out["thresholds"] = {"reference": "SelectorThresholds{} (selector.hpp:16-22)",
-                         "b200": "calibrate_thresholds on the full cfg3 sweep (t_parallel_avg 8)"}
+                         "b200": "calibrate_thresholds on the full cfg3 sweep (t_parallel_avg 16, profiles/r02f_sweep_summary.json)"}
     out["seconds"] = round(time.time() - t0, 1)
     return out
 

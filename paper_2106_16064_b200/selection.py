@@ -277,10 +277,13 @@ class CalibrationRecord:
 # calibrate_thresholds on the B200 sweep (profiles/r01n_sweep*: uniform /
 # banded / heavy R-MAT 2^18..2^22, N = 1..128): once par-rs got its hub path
 # and narrow-row virtual lanes it wins most N <= 4 cells with avg_row >= 8, so
-# the crossover moves from the reference's 32 to 8 (mean per-N selection loss
-# 6.3 % -> 2.5 %, the same on a held-out split).  The reference's defaults
-# stay the default everywhere (bit-exact choices); pass these explicitly.
-B200_THRESHOLDS = SelectorThresholds(4, 8.0, 1.0)
+# the crossover moved from the reference's 32 to 8 in round 1 (mean per-N
+# selection loss 6.3 % -> 2.5 %).  Round 2 (lane-per-job seq sweeps at N = 8 /
+# 16 / 32, streaming par-ws at N <= 2): the calibration moves it to 16 (5.5 %
+# -> 2.3 %, held-out 2.2 %; profiles/r02f_sweep_summary.json).  The
+# reference's defaults stay the default everywhere (bit-exact choices); pass
+# these explicitly.
+B200_THRESHOLDS = SelectorThresholds(4, 16.0, 1.0)
 
 
 def _calibration_loss(cells, t: SelectorThresholds) -> float:
