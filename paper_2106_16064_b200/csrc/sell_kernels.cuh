@@ -196,7 +196,8 @@ struct SellArgs {
 constexpr int kSellStage = 4096;  // one step's 32 G dense rows of CW floats in the ring
 template <int CW, int S, int C>
 __host__ __device__ constexpr int sell_warp_bytes() {
-  return S * kSellStage + C * sell_step_ints(CW) * 4;
+  // row ring + step ring + the output codes of the slice being stored
+  return S * kSellStage + C * sell_step_ints(CW) * 4 + sell_step_ints(CW) * 2;
 }
 template <int CW, int S, int C, int WPC>
 __host__ __device__ constexpr int sell_smem_bytes() {
@@ -334,20 +335,39 @@ seq_sell_kernel(const SellArgs a) {
   for (int g = 0; g < G; ++g) out[g] = -1, len[g] = 0;
   int crem = 0, t = 0;  // steps left in the slice, position in it
   const size_t ystride = (size_t)a.N;
-  auto epilogue = [&]() {
+  // Epilogue of a slice: its 32 G rows go through a free ring stage (the one
+  // of the header step, whose position gathers no rows) so the stores are
+  // coalesced like the gathers: each STG.128 writes 4 G whole rows (storing
+  // from registers, 32 rows of 16 B per instruction, cost ~35 us at cfg2).
+  int* ocode = reinterpret_cast<int*>(wb + S * kSellStage + C * SI * 4);  // [JPS]
+  auto epilogue = [&](int slot) {
+    unsigned char* stg = wb + slot * kSellStage;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if (out[g] == -1) continue;
-      float* base =
-          (out[g] >= 0 ? a.Y + (size_t)out[g] * ystride : a.H + (size_t)(out[g] & 0x7fffffff) * ystride) + col0;
+      ocode[g * 32 + lane] = out[g];
 #pragma unroll
       for (int c = 0; c < CPR; ++c) {
-        const int k = (c + rot) & (CPR - 1);  // slot c holds chunk (c + rot) % CPR
         const float* o = &acc[g][4 * c];
-        if (out[g] >= 0) st_y4(base + 4 * k, o[0], o[1], o[2], o[3]);
-        else *reinterpret_cast<float4*>(base + 4 * k) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(stg + roff[g][c]) = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = 8 * q + i;  // the row this lane's 16-byte chunk ch belongs to (producer mapping)
+      const int oc = ocode[r];
+#ifdef SELL_NO_STORE  // dev experiment (wrong results)
+      if (oc != -5) continue;
+#endif
+      if (oc == -1) continue;
+      const float4 v = *reinterpret_cast<const float4*>(stg + r * RB + ch * 16);
+      if (oc >= 0) {
+        st_y4(a.Y + (size_t)oc * ystride + col0 + ch * 4, v.x, v.y, v.z, v.w);
+      } else {
+        *reinterpret_cast<float4*>(a.H + (size_t)(oc & 0x7fffffff) * ystride + col0 + ch * 4) = v;
+      }
+    }
+    __syncwarp();
   };
 
   // Main loop (S, C powers of two): iteration it consumes the step at virtual
@@ -387,11 +407,18 @@ seq_sell_kernel(const SellArgs a) {
       }
     }
     const int f = map(k + C - 1);
+#ifdef SELL_PF
+    {  // A steps are streamed once from HBM: pull position k + SELL_PF into L2
+      const int pf = map(k + SELL_PF);
+      if (pf >= 0 && lane < SI / 32)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(steps + (size_t)pf * SI + lane * 32));
+    }
+#endif
     // consumer: position k
     const int* cw = cr + (it & (C - 1)) * SI;
     if (crem == 0) {  // header: finish the previous slice, start the next
       ++nslices;
-      epilogue();
+      epilogue(it & (S - 1));  // this position's row stage is free (a header gathers nothing)
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         out[g] = cw[g * 32 + lane];
@@ -406,7 +433,11 @@ seq_sell_kernel(const SellArgs a) {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const float v = __int_as_float(cw[JPS + g * 32 + lane]);
+#ifdef SELL_NO_FP  // dev experiment (wrong results)
+        if (t < len[g] && v == 1234.5f) {
+#else
         if (t < len[g]) {  // padding positions add nothing (also when X holds inf / NaN)
+#endif
 #pragma unroll
           for (int c = 0; c < CPR; ++c) {
             const float4 x = *reinterpret_cast<const float4*>(xrow + roff[g][c]);
@@ -424,15 +455,24 @@ seq_sell_kernel(const SellArgs a) {
       const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       const unsigned d = xdst0 + ((it + S - 1) & (S - 1)) * kSellStage;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
+      for (int i = 0; i < 8; ++i) {
+#ifdef SELL_SKIP_HOT  // dev experiment: upper bound of a hot-row table (wrong results)
+        if (__popc(cc[i]) <= SELL_SKIP_HOT) continue;
+#endif
+#ifdef SELL_NO_GATHER  // dev experiment (wrong results)
+        if (cc[i] != -7) continue;
+#endif
+        cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
+      }
     }
     fetch_step(f, (it + C - 1) & (C - 1));
     cp_commit();
     ++k;
     ++nsteps;
   }
-  epilogue();
   cp_wait<0>();
+  __syncwarp();
+  epilogue(0);
   if (lane == 0) {
     // the last warp out resets the counters for the next call
     __threadfence();
