@@ -190,7 +190,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
     if (sell_rs) {
       SellPlan& sp = get_sell_plan(h, kSellNoChunk, L > 0 ? L : INT32_MAX, cw_rs, s);
       timing_record(1, s);
-      launch_sell(h, sp, d_x, N, d_y, nullptr, s);
+      launch_sell(h, sp, d_x, N, d_y, nullptr, hubs, s);
       timing_record(2, s);
     } else if (id == SPMK_SEQ_ROWSPLIT) {
       const long long TS = h->tune.seq_tile_nnz > 0 ? h->tune.seq_tile_nnz : rs_tile_nnz(h->nnz, N);
@@ -204,7 +204,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       SellPlan& sp = get_sell_plan(h, (long long)cfg.seq_chunk, INT32_MAX, cw_ws, s);
       float* H = sp.nslots > 0 ? h->scratch.get((size_t)sp.nslots * N) : nullptr;
       timing_record(1, s);
-      launch_sell(h, sp, d_x, N, d_y, H, s);
+      launch_sell(h, sp, d_x, N, d_y, H, false, s);
       timing_record(2, s);
     } else {
       const long long CH = (long long)cfg.seq_chunk;

@@ -238,7 +238,9 @@ int sell_width(const spmk_csr_s* h, long long CH, int N, bool aligned);
 constexpr long long kSellNoChunk = 1LL << 40;
 SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStream_t s);
 void free_sell_plan(SellPlan& p);
-void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s);
+// side_busy: a side-stream kernel (seq-rs hub rows) runs concurrently
+void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, bool side_busy,
+                 cudaStream_t s);
 
 // ---- launch_par.cu
 struct ParLaunch {

@@ -273,7 +273,8 @@ void free_sell_plan(SellPlan& p) {
   p = SellPlan{};
 }
 
-void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, cudaStream_t s) {
+void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, float* H, bool side_busy,
+                 cudaStream_t s) {
   const int tiles = N / p.cw;
   SellArgs a{};
   a.steps = p.steps;
@@ -284,6 +285,7 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
   a.Y = Y;
   a.H = H;
   a.N = N;
+  a.claim_first = side_busy ? 1 : 0;
   a.one2 = kOnePair;
   a.trace = sell_trace_buffer(p.nwarps);
   sell_blocks_per_sm(p.cw, p.shape);  // shared-memory opt-in on this device

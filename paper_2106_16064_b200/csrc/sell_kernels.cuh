@@ -189,6 +189,7 @@ struct SellArgs {
   float* __restrict__ Y;          // M x N
   float* __restrict__ H;          // partial slots x N
   int N;
+  int claim_first;                // 1: first chunks claimed per CTA (a concurrent side-stream kernel)
   f32x2 one2;                     // {1, 1}, opaque to ptxas (see f2_add)
   unsigned long long* trace;      // dev: per-warp {start, end, steps, slices} (%globaltimer), or null
 };
@@ -222,7 +223,20 @@ seq_sell_kernel(const SellArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * WPC + warp;
   const int W = gridDim.x * WPC;
-  int* sched = a.sched + 2 * blockIdx.y;  // {chunks claimed beyond the first W, warps done}
+  int* sched = a.sched + 2 * blockIdx.y;  // {chunks claimed, warps done}
+  // First chunks: warp w takes chunk w (the W heaviest, no atomics) unless a
+  // side-stream kernel competes for the SMs (seq-rs hub rows): then one claim
+  // of WPC chunks per CTA, so a CTA that becomes resident late starts on
+  // later, lighter chunks instead of a statically assigned heavy one
+  // (measured: static 187 us at cfg2; claimed 200 us, but seq-rs with hubs
+  // 390 -> 553 us in some runs when static).
+  __shared__ int s_first;
+  int first = w;
+  if (a.claim_first) {
+    if (threadIdx.x == 0) s_first = atomicAdd(sched, WPC);
+    __syncthreads();
+    first = s_first + warp;
+  }
   unsigned long long t_start = 0;
   int nsteps = 0, nslices = 0;
   if (a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -241,9 +255,8 @@ seq_sell_kernel(const SellArgs a) {
   const unsigned n16 = (unsigned)a.N / 4;
   const unsigned xdst0 = xr0 + (unsigned)(q * 8 * RB + ch * 16);
 
-  // Work: chunks of whole slices (plan: a.cstep), heaviest first.  Warp w
-  // starts with chunk w and claims the next one (atomic counter) as soon as
-  // it enters a chunk; the claim and the chunk bounds load are consumed only
+  // Work: chunks of whole slices (plan: a.cstep), heaviest first.  A warp
+  // claims the next chunk (atomic counter) as soon as it enters one; the claim and the chunk bounds load are consumed only
   // when the step ring reaches the chunk end (every chunk but the last has
   // >= C steps, so the rings never run more than one chunk ahead).
   int a0 = 0, alen = 0;                   // chunk the consumer is in (real start, steps)
@@ -251,7 +264,7 @@ seq_sell_kernel(const SellArgs a) {
   int pc0 = 0, pc1 = 0;                   // lane 0: the claim's bounds
   auto claim = [&]() {
     if (lane == 0) {
-      const int c = atomicAdd(sched, 1) + W;
+      const int c = atomicAdd(sched, 1) + (a.claim_first ? 0 : W);
       pc0 = c < a.nchunks ? a.cstep[c] : 0;
       pc1 = c < a.nchunks ? a.cstep[c + 1] : 0;
     }
@@ -270,19 +283,27 @@ seq_sell_kernel(const SellArgs a) {
     resolve();
     return v - alen < blen ? b0 + (v - alen) : -1;
   };
-  if (w < a.nchunks) {
-    a0 = a.cstep[w];
-    alen = a.cstep[w + 1] - a0;
+  if (first < a.nchunks) {
+    a0 = a.cstep[first];
+    alen = a.cstep[first + 1] - a0;
     claim();
   } else {
     blen = 0;
   }
 
-  // step g into step-ring slot cs: SI / 4 lanes' worth of 16-byte copies
+  // step g into step-ring slot cs: every lane copies SI / 32 ints (8-byte
+  // copies at CW = 32, 16-byte ones below: no lane predicate)
   auto fetch_step = [&](int g, int cs) {
     if (g < 0) return;
+    if constexpr (SI / 32 == 2) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(cr0 + (cs * SI + lane * 2) * 4),
+                   "l"(steps + (size_t)g * SI + lane * 2)
+                   : "memory");
+    } else {
 #pragma unroll
-    for (int o = lane; o < SI / 4; o += 32) cp16(cr0 + (cs * SI + o * 4) * 4, steps + (size_t)g * SI + o * 4);
+      for (int o = 0; o < SI / 128; ++o)
+        cp16(cr0 + (cs * SI + (o * 32 + lane) * 4) * 4, steps + (size_t)g * SI + (o * 32 + lane) * 4);
+    }
   };
   int prem = 0;  // producer: data steps left in the current slice
   // dense rows of step p (step slot pcs) into row-ring slot pxs (prologue)
@@ -392,7 +413,10 @@ seq_sell_kernel(const SellArgs a) {
     __syncwarp();
     // producer, part 1: the columns of position k + S - 1 (smem loads issued
     // now, consumed after the consumer's work)
-    const int p = map(k + S - 1);
+    // positions k + S - 1 and k + C - 1: inside the consumer's chunk except
+    // in its last C - 1 iterations (chunks are >= C steps)
+    const bool inside = k + C - 1 < alen;
+    const int p = inside ? a0 + k + S - 1 : map(k + S - 1);
     const int pcs = (it + S - 1) & (C - 1);
     bool issue = false;
     int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
@@ -406,7 +430,7 @@ seq_sell_kernel(const SellArgs a) {
         c1 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q + 1];
       }
     }
-    const int f = map(k + C - 1);
+    const int f = inside ? a0 + k + C - 1 : map(k + C - 1);
 #ifdef SELL_PF
     {  // A steps are streamed once from HBM: pull position k + SELL_PF into L2
       const int pf = map(k + SELL_PF);
