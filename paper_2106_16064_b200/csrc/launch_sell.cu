@@ -43,19 +43,19 @@ const SellShape kSellShapes[3][kSellShapeCount] = {
         sell_shape<32, 4, 8, 4, 3>(),   // 0: 12 warps / SM, 3 steps of rows in flight per warp
         sell_shape<32, 2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
         sell_shape<32, 4, 8, 12, 1>(),  // 2: 12 warps in one CTA
-        sell_shape<32, 8, 16, 3, 2>(),  // 3: 6 warps, 7 in flight
+        sell_shape<32, 3, 6, 4, 4>(),   // 3: 16 warps, 2 in flight
     },
     {
         sell_shape<16, 4, 8, 5, 2>(),   // 0: 10 warps / SM
         sell_shape<16, 2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
         sell_shape<16, 4, 8, 4, 2>(),   // 2: 8 warps
-        sell_shape<16, 4, 8, 3, 3>(),   // 3: 9 warps
+        sell_shape<16, 3, 6, 4, 3>(),   // 3: 12 warps, 2 in flight
     },
     {
         sell_shape<8, 4, 8, 3, 3>(),    // 0: 9 warps / SM
         sell_shape<8, 2, 4, 8, 2>(),    // 1: 16 warps, 1 in flight
         sell_shape<8, 4, 8, 4, 2>(),    // 2: 8 warps
-        sell_shape<8, 2, 4, 6, 3>(),    // 3: 18 warps, 1 in flight
+        sell_shape<8, 3, 6, 4, 3>(),    // 3: 12 warps, 2 in flight
     },
 };
 int cw_index(int cw) { return cw == 32 ? 0 : (cw == 16 ? 1 : 2); }

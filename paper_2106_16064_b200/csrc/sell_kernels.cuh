@@ -209,7 +209,7 @@ template <int CW, int S, int C, int WPC, int MINB>
 __global__ void __launch_bounds__(WPC * 32, MINB)
 seq_sell_kernel(const SellArgs a) {
   static_assert(CW == 8 || CW == 16 || CW == 32, "column width");
-  static_assert(S >= 2 && C >= 2 * S - 1 && (S & (S - 1)) == 0 && (C & (C - 1)) == 0, "ring depths");
+  static_assert(S >= 2 && C >= 2 * S - 1, "ring depths");
   constexpr int G = 32 / CW;           // jobs per lane
   constexpr int JPS = 32 * G;          // jobs per slice = dense rows per step
   constexpr int SI = 2 * JPS;          // ints per step
@@ -391,7 +391,7 @@ seq_sell_kernel(const SellArgs a) {
     __syncwarp();
   };
 
-  // Main loop (S, C powers of two): iteration it consumes the step at virtual
+  // Main loop: iteration it consumes the step at virtual
   // position k from step slot it % C and row slot it % S, produces the rows
   // of position k + S - 1 and fetches position k + C - 1 into the slots the
   // previous iteration consumed.
@@ -417,7 +417,7 @@ seq_sell_kernel(const SellArgs a) {
     // in its last C - 1 iterations (chunks are >= C steps)
     const bool inside = k + C - 1 < alen;
     const int p = inside ? a0 + k + S - 1 : map(k + S - 1);
-    const int pcs = (it + S - 1) & (C - 1);
+    const int pcs = (int)((unsigned)(it + S - 1) % C);
     bool issue = false;
     int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
     if (p >= 0) {
@@ -439,10 +439,10 @@ seq_sell_kernel(const SellArgs a) {
     }
 #endif
     // consumer: position k
-    const int* cw = cr + (it & (C - 1)) * SI;
+    const int* cw = cr + (int)((unsigned)it % C) * SI;
     if (crem == 0) {  // header: finish the previous slice, start the next
       ++nslices;
-      epilogue(it & (S - 1));  // this position's row stage is free (a header gathers nothing)
+      epilogue((int)((unsigned)it % S));  // this position's row stage is free (a header gathers nothing)
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         out[g] = cw[g * 32 + lane];
@@ -453,7 +453,7 @@ seq_sell_kernel(const SellArgs a) {
       crem = cw[JPS];  // position 0 holds the slice's longest job
       t = 0;
     } else {
-      const unsigned char* xrow = wb + (it & (S - 1)) * kSellStage;
+      const unsigned char* xrow = wb + (int)((unsigned)it % S) * kSellStage;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const float v = __int_as_float(cw[JPS + g * 32 + lane]);
@@ -477,7 +477,7 @@ seq_sell_kernel(const SellArgs a) {
     // step of position k + C - 1 into the step slot, that position k - 1 used
     if (issue) {
       const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-      const unsigned d = xdst0 + ((it + S - 1) & (S - 1)) * kSellStage;
+      const unsigned d = xdst0 + (int)((unsigned)(it + S - 1) % S) * kSellStage;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
 #ifdef SELL_SKIP_HOT  // dev experiment: upper bound of a hot-row table (wrong results)
@@ -489,7 +489,7 @@ seq_sell_kernel(const SellArgs a) {
         cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
       }
     }
-    fetch_step(f, (it + C - 1) & (C - 1));
+    fetch_step(f, (int)((unsigned)(it + C - 1) % C));
     cp_commit();
     ++k;
     ++nsteps;
