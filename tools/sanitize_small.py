@@ -1,4 +1,6 @@
-"""Dev: every variant once on small matrices (for compute-sanitizer runs)."""
+"""Dev: every variant once on small matrices (for compute-sanitizer runs),
+including the lane-per-job sweep at every width and shape and the hub-row
+kernels on most rows."""
 import os
 import sys
 
@@ -9,16 +11,25 @@ import paper_2106_16064_b200 as spmk  # noqa: E402
 
 for skew in ((0.57, 0.19, 0.19, 0.05), (0.25, 0.25, 0.25, 0.25)):
     d = spmk.DeviceCsr.generate_rmat(10, 8, skew, 3)
-    for n in (1, 3, 4, 32, 64):
+    for n in (1, 3, 4, 8, 16, 32, 64):
         x = spmk.make_dense_device(d.num_cols, n, 5 + n)
         for kid in spmk.kAllKernels:
             for cfg in (None, spmk.KernelConfig(lane_width=8, seq_chunk=16)):
                 d.spmm(kid, x, cfg=cfg)
                 if kid in (spmk.kParRowSplit, spmk.kSeqRowSplit):  # hub-row kernels on most rows
-                    os.environ["SPMK_HUB_NNZ"] = "8"
+                    d.set_tuning("hub_nnz", 8)
                     d.spmm(kid, x, cfg=cfg)
-                    os.environ["SPMK_HUB_TWO_PASS"] = "0"
+                    d.set_tuning("hub_two_pass", 0)
                     d.spmm(kid, x, cfg=cfg)
-                    del os.environ["SPMK_HUB_TWO_PASS"], os.environ["SPMK_HUB_NNZ"]
+                    d.set_tuning("hub_two_pass", -1)
+                    d.set_tuning("hub_nnz", -1)
+                if kid in (spmk.kSeqBalanced, spmk.kSeqRowSplit) and n in (8, 16, 32, 64):
+                    for shape in (1, 2, 3):
+                        d.set_tuning("sell_cfg", shape)
+                        d.spmm(kid, x, cfg=cfg)
+                    d.set_tuning("sell_cfg", 0)
+                    d.set_tuning("seq_impl", 3)
+                    d.spmm(kid, x, cfg=cfg)
+                    d.set_tuning("seq_impl", 2)
     torch.cuda.synchronize()
 print("sanitize run ok")
