@@ -82,13 +82,31 @@ __device__ __forceinline__ float4 ld_stream4(const float* ptr, uint64_t pol) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
   return v;
 }
-// X gathers: read-only path, normal L1 allocation (hub columns repeat).
-__device__ __forceinline__ float ld_x(const float* p) { return __ldg(p); }
+// X gathers: read-only path, normal L1 allocation (hub columns repeat), and
+// an L2 evict-last priority against the evict-first A stream, so the dense
+// operand keeps its L2 lines when it does not fit (measured on B200: cfg5
+// par-ws 2.73 -> 2.57 ms, par-rs 3.11 -> 3.05 ms).
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float ld_x(const float* p) {
+  float v;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(evict_last_policy()));
+  return v;
+}
 __device__ __forceinline__ float2 ld_x2(const float* p) {
-  return __ldg(reinterpret_cast<const float2*>(p));
+  float2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(evict_last_policy()));
+  return v;
 }
 __device__ __forceinline__ float4 ld_x4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
+  float4 v;
+  asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p), "l"(evict_last_policy()));
+  return v;
 }
 // Y is written once: streaming store.
 __device__ __forceinline__ void st_y(float* p, float v) { __stcs(p, v); }
