@@ -150,7 +150,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
   // seq-ws / seq-rs at N = 32: the lane-per-job sweep (it writes the empty
   // rows itself); seq-rs rows of >= L nonzeros go to the hub kernels
   const int cw_ws = id == SPMK_SEQ_BALANCED ? sell_width(h, (long long)cfg.seq_chunk, N, aligned) : 0;
-  const int cw_rs = id == SPMK_SEQ_ROWSPLIT ? sell_width(h, 1, N, aligned) : 0;
+  const int cw_rs = id == SPMK_SEQ_ROWSPLIT ? sell_width(h, kSellNoChunk, N, aligned) : 0;
   const bool sell_ws = cw_ws > 0, sell_rs = cw_rs > 0;
   const bool sell = sell_ws || sell_rs;
   const bool rs = id == SPMK_PAR_ROWSPLIT || id == SPMK_SEQ_ROWSPLIT;
@@ -453,7 +453,7 @@ spmk_status spmk_spmm_path(spmk_csr_t a, spmk_kernel_id id, const spmk_kernel_co
   const spmk_kernel_config c = cfg_or_default(cfg);
   const bool ok = n > 0 && n <= INT32_MAX;
   *path = ok && ((id == SPMK_SEQ_BALANCED && spmk_host::sell_width(a, (long long)c.seq_chunk, (int)n, true) > 0) ||
-                 (id == SPMK_SEQ_ROWSPLIT && spmk_host::sell_width(a, 1, (int)n, true) > 0))
+                 (id == SPMK_SEQ_ROWSPLIT && spmk_host::sell_width(a, spmk_host::kSellNoChunk, (int)n, true) > 0))
               ? 1
               : 0;
   return SPMK_OK;

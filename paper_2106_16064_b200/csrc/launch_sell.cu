@@ -19,6 +19,7 @@ namespace {
 
 constexpr int kSellChunkMin = 16, kSellChunkMax = 512;  // work-queue chunk sizes (steps; >= C)
 constexpr int kSellMaxTiles = 64;                        // column tiles (N <= 2048)
+constexpr unsigned long long kSellMaxXBytes = 768ull << 20;  // seq-ws default: X up to 768 MB
 // Sweep shapes (ring depths S / C, warps per CTA, CTAs per SM); tuning knob
 // sell_cfg picks one (measured on B200).
 struct SellShape {
@@ -147,9 +148,15 @@ int sell_width(const spmk_csr_s* h, long long CH, int N, bool aligned) {
   // tiles of wider X only with seq_impl 3
   if (h->tune.seq_impl < 2) return 0;
   int cw = 0;
+  // seq-ws with an X far beyond L2 (DRAM-bound gathers): the tile sweep's
+  // row-order locality wins (R-MAT s24 e32: N = 16 / 32 tile 4.9 / 7.0 ms vs
+  // 5.8 / 8.0; X 1.07 / 2.1 GB), below it the sweep (s22 N = 32, X 537 MB:
+  // 830 vs 934 us; s24 N = 8, X 537 MB: 3.6 vs 4.3 ms); seq-rs always
+  const bool big_x = CH != kSellNoChunk && (unsigned long long)h->k * N * 4 > kSellMaxXBytes;
+  if (h->tune.seq_impl == 2 && big_x) return 0;
   if (N == 32 || N == 16 || N == 8) cw = N;
   else if (h->tune.seq_impl == 3 && N % 32 == 0 && N / 32 <= kSellMaxTiles) cw = 32;
-  const bool ok = cw > 0 && aligned && CH <= kSellMaxChunk && h->k < INT32_MAX &&
+  const bool ok = cw > 0 && aligned && (CH <= kSellMaxChunk || CH == kSellNoChunk) && h->k < INT32_MAX &&
                   (unsigned long long)h->k * (unsigned long long)(N / 4) < (1ull << 32) && h->nnz < INT32_MAX &&
                   h->m < INT32_MAX;
   return ok ? cw : 0;
