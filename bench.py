@@ -447,6 +447,8 @@ def selection_loss_summary():
     t0 = time.time()
     recs = {"reference": [], "b200": []}
     ns = (1, 2, 4, 8, 16, 32, 64, 128)
+    per_n = {}
+    peak, _ = peaks()
     for name, a in inputs.sweep_corpus(scales=(18, 20)):
         for n in ns:
             x = make_dense_device(a.num_cols, n, DENSE_SEED + n)
@@ -458,6 +460,13 @@ def selection_loss_summary():
             for key, t in (("reference", SelectorThresholds()), ("b200", B200_THRESHOLDS)):
                 chosen = a.select(n, t)
                 recs[key] += cell + [BenchRecord(**{**cell[chosen.index].__dict__, "selected_by_rule": True})]
+            if name == "rmat-heavy-s20-e16":  # the cfg2 matrix: the metric's "at N = 1..128" row
+                chosen = a.select(n)
+                r = cell[chosen.index]
+                comp = 4 * (a.num_rows + 1) + 8 * a.nnz + 4 * a.num_cols * n + 4 * a.num_rows * n
+                per_n[str(n)] = {"kernel": chosen.name, "gflops": round(r.gflops, 1),
+                                 "us": round(r.time_seconds * 1e6, 1),
+                                 "roofline_frac": round(comp / r.time_seconds / 1e9 / peak, 4)}
             del x
         del a
         torch.cuda.empty_cache()
@@ -467,6 +476,9 @@ def selection_loss_summary():
         out[key] = {"mean_per_n_loss": round(mean_per_n_loss(s), 4),
                     "per_n_loss": {str(k): round(v, 4) for k, v in s.per_n_loss.items()},
                     "best_single_kernel_loss": round(min_single_kernel_loss(s), 4)}
+    out["cfg2_matrix_per_n"] = {"matrix": "R-MAT s20 e16 heavy seed 1 (cfg2)", "selected_by": "select_kernel (reference thresholds)",
+                                "roofline": "compulsory bytes 4(M+1) + 8 nnz + 4 K N + 4 M N over measured HBM, whole call",
+                                "n": per_n}
     out["cells"] = len(recs["reference"]) // 5
     out["sweep"] = "uniform/banded/heavy x 2^18, 2^20 x N=1..128 (reduced cfg3), median of 3, L2 flushed"
     out["thresholds"] = {"reference": "SelectorThresholds{} (selector.hpp:16-22)",
@@ -554,10 +566,12 @@ def main():
     if G == 1:
         step_bytes = 4 * (M + 1) + 8 * a.nnz + 4 * K * n + 4 * M * n
         result["run"]["effective_GBps_compulsory"] = round(step_bytes / (r["ms_per_step"] * 1e-3) / 1e9, 1)
-    if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(a, x, r["kid"], n, name)
+    # the reference's call shape first: host-side copies, timed before the
+    # CPU baseline loads the reference library and its worker threads
     if rank == 0 and G == 1 and not args.no_extras:
         result["call_shapes"] = call_shapes(a, x, r["kid"]) if name == "cfg2" else None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(a, x, r["kid"], n, name)
     del r, a, x
     torch.cuda.empty_cache()
     if G == 1 and name == "cfg2" and not args.no_extras:

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -420,6 +421,9 @@ spmk_status spmk_spmm_csr_host(int64_t num_rows, int64_t num_cols, int64_t nnz,
   spmk_csr_t h = nullptr;
   st = spmk_csr_create(num_rows, num_cols, nnz, row_ptr, col_idx, values, device, &h);
   if (st != SPMK_OK) return st;
+  // One call per handle: the lane-per-job layout (a sorted copy of A) could
+  // not be amortised, so the tile sweeps run unless SPMK_SEQ_IMPL asks.
+  if (!std::getenv("SPMK_SEQ_IMPL")) h->tune.seq_impl = 1;
   st = spmk_spmm_host(h, id, cfg, x, n, y, nullptr);
   spmk_csr_destroy(h);
   return st;
