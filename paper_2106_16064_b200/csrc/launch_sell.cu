@@ -265,7 +265,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStrea
   CK(cudaMemcpyAsync(p.cstep, cs.data(), sizeof(int) * cs.size(), cudaMemcpyHostToDevice, s));
   p.sched = dev_alloc<int>(2 * kSellMaxTiles);
   CK(cudaMemsetAsync(p.sched, 0, sizeof(int) * 2 * kSellMaxTiles, s));
-  sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, jps, step_ex.p, jstart.p, jout.p,
+  sell_fill_kernel<<<grid_for((long long)nsl * 32), 256, 0, s>>>(sidx.p, slen.p, J, nsl, jps, cw == 32 ? 0 : 512 / (4 * cw), step_ex.p, jstart.p, jout.p,
                                                                  h->col, h->val, p.steps); LAUNCHED(1);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));  // temporaries (and cs) are freed on return

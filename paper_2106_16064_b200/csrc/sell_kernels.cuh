@@ -132,6 +132,7 @@ __global__ void sell_slice_kernel(const int* __restrict__ slen_sorted, int nsl, 
 // One warp per slice (jps = 32 G jobs: position g * 32 + lane): header + data
 // steps of 2 jps ints.
 __global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __restrict__ slen, int J, int nsl, int jps,
+                                 int rpi,
                                  const long long* __restrict__ step_ex, const int* __restrict__ jstart,
                                  const int* __restrict__ jout,
                                  const int* __restrict__ col, const float* __restrict__ val, int* __restrict__ out) {
@@ -140,6 +141,10 @@ __global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __rest
        s += ((long long)gridDim.x * blockDim.x) >> 5) {
     const int L = slen[(long long)jps * s];
     int* p = out + step_ex[s] * 2 * jps;
+    // column of position pos at its producer index (see seq_sell_kernel: at
+    // CW < 32 an LDGSTS copies rpi consecutive ring rows, lane group g needs
+    // rows g, rpi + g, ...: stored contiguously)
+    auto cidx = [&](int pos) { return rpi ? (pos % rpi) * 8 + pos / rpi : pos; };
     for (int pos = lane; pos < jps; pos += 32) {
       const long long j = (long long)jps * s + pos;
       const bool ok = j < J;
@@ -151,7 +156,7 @@ __global__ void sell_fill_kernel(const int* __restrict__ sidx, const int* __rest
       for (int t = 0; t < L; ++t) {
         int* q = p + (long long)(t + 1) * 2 * jps;
         const bool in = t < len;
-        q[pos] = in ? col[st + t] : 0;
+        q[cidx(pos)] = in ? col[st + t] : 0;
         q[jps + pos] = in ? __float_as_int(val[st + t]) : 0;
       }
     }
@@ -247,13 +252,17 @@ seq_sell_kernel(const SellArgs a) {
   const unsigned cr0 = xr0 + S * kSellStage;
   const int col0 = blockIdx.y * CW;
   const int* steps = a.steps;
-  // LDGSTS lanes: group q = lane / LPR copies rows 8 q + i (i = 0..7), 16-byte
-  // chunk lane % LPR: every instruction moves 512 contiguous-per-row bytes
+  // LDGSTS lanes: group q = lane / LPR copies chunk lane % LPR of 8 rows, one
+  // per instruction: rows 8 q + i at CW = 32 (4 rows 1 KB apart: 4 wavefronts,
+  // the minimum), rows i RPI + q below (the instruction's RPI rows contiguous;
+  // 8 q + i there put 16 / 8 rows on the same banks: 16- / 8-way conflicts)
   const int q = lane / LPR, ch = lane % LPR;
   // 32-bit row offsets in 16-byte units (the plan checks K * N / 4 < 2^32)
   const float4* xg = reinterpret_cast<const float4*>(a.X + col0);
   const unsigned n16 = (unsigned)a.N / 4;
-  const unsigned xdst0 = xr0 + (unsigned)(q * 8 * RB + ch * 16);
+  constexpr int RPI = 512 / RB;                       // rows per LDGSTS instruction
+  constexpr int ISTRIDE = CW == 32 ? RB : 512;         // ring bytes between a lane's rows
+  const unsigned xdst0 = xr0 + (unsigned)((CW == 32 ? q * 8 * RB : q * RB) + ch * 16);
 
   // Work: chunks of whole slices (plan: a.cstep), heaviest first.  A warp
   // claims the next chunk (atomic counter) as soon as it enters one; the claim and the chunk bounds load are consumed only
@@ -319,7 +328,7 @@ seq_sell_kernel(const SellArgs a) {
     const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
     const unsigned d = xdst0 + pxs * kSellStage;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
+    for (int i = 0; i < 8; ++i) cp16(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch));
   };
 
   // prologue: steps 0 .. C-2 (one group each), then rows of steps 0 .. S-2
@@ -375,7 +384,7 @@ seq_sell_kernel(const SellArgs a) {
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int r = 8 * q + i;  // the row this lane's 16-byte chunk ch belongs to (producer mapping)
+      const int r = CW == 32 ? 8 * q + i : i * RPI + q;  // this lane's row (producer mapping)
       const int oc = ocode[r];
 #ifdef SELL_NO_STORE  // dev experiment (wrong results)
       if (oc != -5) continue;
@@ -486,7 +495,7 @@ seq_sell_kernel(const SellArgs a) {
 #ifdef SELL_NO_GATHER  // dev experiment (wrong results)
         if (cc[i] != -7) continue;
 #endif
-        cp16(d + i * RB, xg + ((unsigned)cc[i] * n16 + ch));
+        cp16(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch));
       }
     }
     fetch_step(f, (int)((unsigned)(it + C - 1) % C));
