@@ -48,15 +48,15 @@ const SellShape kSellShapes[3][kSellShapeCount] = {
     },
     {
         sell_shape<16, 4, 8, 5, 2>(),   // 0: 10 warps / SM
-        sell_shape<16, 2, 4, 8, 2>(),   // 1: 16 warps, 1 in flight
-        sell_shape<16, 4, 8, 4, 2>(),   // 2: 8 warps
+        sell_shape<16, 3, 5, 4, 3>(),   // 1: 12 warps, 2 in flight
+        sell_shape<16, 4, 7, 5, 2>(),   // 2: 10 warps, shorter step ring
         sell_shape<16, 3, 6, 4, 3>(),   // 3: 12 warps, 2 in flight
     },
     {
         sell_shape<8, 4, 8, 3, 3>(),    // 0: 9 warps / SM
-        sell_shape<8, 2, 4, 8, 2>(),    // 1: 16 warps, 1 in flight
-        sell_shape<8, 4, 8, 4, 2>(),    // 2: 8 warps
-        sell_shape<8, 3, 6, 4, 3>(),    // 3: 12 warps, 2 in flight
+        sell_shape<8, 3, 5, 4, 3>(),    // 1: 12 warps, 2 in flight
+        sell_shape<8, 4, 7, 3, 3>(),    // 2: 9 warps, shorter step ring
+        sell_shape<8, 3, 5, 5, 2>(),    // 3: 10 warps, 2 in flight
     },
 };
 int cw_index(int cw) { return cw == 32 ? 0 : (cw == 16 ? 1 : 2); }
