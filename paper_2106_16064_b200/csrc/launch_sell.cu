@@ -17,9 +17,10 @@ using namespace spmk_dev;
 namespace spmk_host {
 namespace {
 
-// Work-queue chunk sizes in steps: >= every shape's C (the rings run at most
-// one chunk ahead); 8 measured 1.5 % faster than 16 at cfg2 (finer tail).
-constexpr int kSellChunkMin = 8, kSellChunkMax = 512;
+// Work-queue chunk sizes in steps: >= every shape's S + C - 1 (the rings run
+// at most one chunk ahead, and the sweep resolves the next chunk once per S
+// steps); the smallest allowed measured best at cfg2 (finer tail).
+constexpr int kSellChunkMin = 12, kSellChunkMax = 512;
 constexpr int kSellGuide = 4;  // target chunk = remaining steps / (kSellGuide x warps)
 constexpr int kSellMaxTiles = 64;                        // column tiles (N <= 2048)
 constexpr unsigned long long kSellMaxXBytes = 768ull << 20;  // seq-ws default: X up to 768 MB
@@ -51,15 +52,15 @@ const SellShape kSellShapes[3][kSellShapeCount] = {
     },
     {
         sell_shape<16, 4, 8, 5, 2>(),   // 0: 10 warps / SM
-        sell_shape<16, 3, 5, 4, 3>(),   // 1: 12 warps, 2 in flight
-        sell_shape<16, 4, 7, 5, 2>(),   // 2: 10 warps, shorter step ring
-        sell_shape<16, 3, 6, 4, 3>(),   // 3: 12 warps, 2 in flight
+        sell_shape<16, 3, 6, 4, 3>(),   // 1: 12 warps, 2 in flight
+        sell_shape<16, 2, 4, 8, 2>(),   // 2: 16 warps, 1 in flight
+        sell_shape<16, 3, 6, 5, 2>(),   // 3: 10 warps, 2 in flight
     },
     {
         sell_shape<8, 4, 8, 3, 3>(),    // 0: 9 warps / SM
-        sell_shape<8, 3, 5, 4, 3>(),    // 1: 12 warps, 2 in flight
-        sell_shape<8, 4, 7, 3, 3>(),    // 2: 9 warps, shorter step ring
-        sell_shape<8, 3, 5, 5, 2>(),    // 3: 10 warps, 2 in flight
+        sell_shape<8, 3, 6, 4, 3>(),    // 1: 12 warps, 2 in flight
+        sell_shape<8, 2, 4, 8, 2>(),    // 2: 16 warps, 1 in flight
+        sell_shape<8, 3, 6, 5, 2>(),    // 3: 10 warps, 2 in flight
     },
 };
 int cw_index(int cw) { return cw == 32 ? 0 : (cw == 16 ? 1 : 2); }
@@ -295,6 +296,7 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
   a.Y = Y;
   a.H = H;
   a.N = N;
+  a.K = (int)std::min<long long>(h->k, 1 << 30);
   a.claim_first = side_busy ? 1 : 0;
   a.one2 = kOnePair;
   a.trace = sell_trace_buffer(p.nwarps);

@@ -48,6 +48,8 @@
 // tile sweep of seq_kernels.cuh spends ~7.5 warp instructions per nonzero on
 // them).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace spmk_dev {
@@ -168,7 +170,33 @@ __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)
 __device__ __forceinline__ void cp16(unsigned dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+// predicated forms: a predicate instead of a branch around the copy
+__device__ __forceinline__ void cp16_if(unsigned dst, const void* src, bool on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.cg.shared.global [%0], [%1], 16;\n}" ::"r"(dst),
+               "l"(src), "r"((int)on)
+               : "memory");
+}
+__device__ __forceinline__ void cp8_if(unsigned dst, const void* src, bool on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 8;\n}" ::"r"(dst),
+               "l"(src), "r"((int)on)
+               : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// U = 0 .. N-1 in order as compile-time constants, stopping at the first false
+template <int U, int N>
+struct SellUnroll {
+  template <class F, class P>
+  __device__ __forceinline__ static bool run(F& f, P p) {
+    return f(std::integral_constant<int, U>{}, p) && SellUnroll<U + 1, N>::run(f, p);
+  }
+};
+template <int N>
+struct SellUnroll<N, N> {
+  template <class F, class P>
+  __device__ __forceinline__ static bool run(F&, P) {
+    return true;
+  }
+};
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -194,6 +222,7 @@ struct SellArgs {
   float* __restrict__ Y;          // M x N
   float* __restrict__ H;          // partial slots x N
   int N;
+  int K;                          // rows of X (0: no X row 0 to test)
   int claim_first;                // 1: first chunks claimed per CTA (a concurrent side-stream kernel)
   f32x2 one2;                     // {1, 1}, opaque to ptxas (see f2_add)
   unsigned long long* trace;      // dev: per-warp {start, end, steps, slices} (%globaltimer), or null
@@ -214,7 +243,7 @@ template <int CW, int S, int C, int WPC, int MINB>
 __global__ void __launch_bounds__(WPC * 32, MINB)
 seq_sell_kernel(const SellArgs a) {
   static_assert(CW == 8 || CW == 16 || CW == 32, "column width");
-  static_assert(S >= 2 && C >= 2 * S - 1, "ring depths");
+  static_assert(S >= 2 && C == 2 * S, "ring depths (the step ring is two halves of S slots)");
   constexpr int G = 32 / CW;           // jobs per lane
   constexpr int JPS = 32 * G;          // jobs per slice = dense rows per step
   constexpr int SI = 2 * JPS;          // ints per step
@@ -347,14 +376,17 @@ seq_sell_kernel(const SellArgs a) {
 
   // This lane's jobs sit at positions g * 32 + lane of a slice; their rows are
   // read in rotated chunk order (chunk (c + rot) % CPR at slot c) so the 8
-  // lanes of a quarter warp hit 8 different bank groups.
+  // lanes of a quarter warp hit 8 different bank groups.  Offsets from s_sell
+  // (this warp's ring included): every row read is one register + a constant.
   constexpr int ROT_SHIFT = CW == 32 ? 0 : (CW == 16 ? 1 : 2);
   const int rot = (lane >> ROT_SHIFT) & (CPR - 1);
+  const unsigned wofs = (unsigned)(warp * sell_warp_bytes<CW, S, C>());
   unsigned roff[G][CPR];
 #pragma unroll
   for (int g = 0; g < G; ++g)
 #pragma unroll
-    for (int c = 0; c < CPR; ++c) roff[g][c] = (unsigned)((g * 32 + lane) * RB + (((c + rot) & (CPR - 1)) * 16));
+    for (int c = 0; c < CPR; ++c)
+      roff[g][c] = wofs + (unsigned)((g * 32 + lane) * RB + (((c + rot) & (CPR - 1)) * 16));
   float acc[G][CW];
 #pragma unroll
   for (int g = 0; g < G; ++g)
@@ -371,7 +403,7 @@ seq_sell_kernel(const SellArgs a) {
   // from registers, 32 rows of 16 B per instruction, cost ~35 us at cfg2).
   int* ocode = reinterpret_cast<int*>(wb + S * kSellStage + C * SI * 4);  // [JPS]
   auto epilogue = [&](int slot) {
-    unsigned char* stg = wb + slot * kSellStage;
+    unsigned char* stg = s_sell + slot * kSellStage;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       ocode[g * 32 + lane] = out[g];
@@ -386,11 +418,8 @@ seq_sell_kernel(const SellArgs a) {
     for (int i = 0; i < 8; ++i) {
       const int r = CW == 32 ? 8 * q + i : i * RPI + q;  // this lane's row (producer mapping)
       const int oc = ocode[r];
-#ifdef SELL_NO_STORE  // dev experiment (wrong results)
-      if (oc != -5) continue;
-#endif
       if (oc == -1) continue;
-      const float4 v = *reinterpret_cast<const float4*>(stg + r * RB + ch * 16);
+      const float4 v = *reinterpret_cast<const float4*>(stg + wofs + r * RB + ch * 16);
       if (oc >= 0) {
         st_y4(a.Y + (size_t)oc * ystride + col0 + ch * 4, v.x, v.y, v.z, v.w);
       } else {
@@ -400,58 +429,60 @@ seq_sell_kernel(const SellArgs a) {
     __syncwarp();
   };
 
-  // Main loop: iteration it consumes the step at virtual
-  // position k from step slot it % C and row slot it % S, produces the rows
-  // of position k + S - 1 and fetches position k + C - 1 into the slots the
-  // previous iteration consumed.
+  // Padding positions gather X row 0 and multiply it by 0: when this tile of
+  // row 0 is finite that adds +-0 to an accumulator that is never -0 (same
+  // bits), so the sweep runs without the per-job length test.
+  bool row0_finite = true;
+  if (a.K > 0) row0_finite = __all_sync(0xffffffffu, isfinite(__ldg(a.X + col0 + lane % CW)));
+
+  // Main loop, in groups of S iterations (C = 2 S).  Iteration u of a group
+  // consumes position k from step slot (half h, u) and row stage u, produces
+  // the rows of position k + S - 1 into stage (u - 1) % S and fetches position
+  // k + C - 1 into the step slot iteration u - 1 consumed; h flips per group.
+  // Every ring address is a register plus a constant, and the only per-step
+  // branch is the consumer's header test: the producer's header / end cases
+  // are predicates, the next chunk is resolved once per group (work chunks
+  // but the last are >= S + C - 1 steps, kSellChunkMin).
+  constexpr unsigned HALF = S * SI * 4;
+  const unsigned cro = wofs + S * kSellStage;  // step ring, from s_sell
+  unsigned hoff = 0;                           // byte offset of half h
   int k = 0;
-#pragma unroll 1
-  for (int it = 0;; ++it) {
-    if (k == alen) {  // the consumer leaves its chunk
-      resolve();
-      if (blen <= 0) break;
-      a0 = b0;
-      alen = blen;
-      k = 0;
-      claim();
-    }
-    // One wait per iteration: all but the last S - 2 cp.async groups are
-    // complete, i.e. the rows of position k (issued S - 1 iterations ago) and
-    // the step of position k + S - 1 (fetched C - 1 steps ahead, C >= 2S - 1).
+  auto step = [&](auto uc, auto chk) -> bool {
+    constexpr int u = decltype(uc)::value;
+    constexpr bool CHECK = decltype(chk)::value;
+    // one wait per iteration: the rows of position k (issued S - 1 iterations
+    // ago) and the step of position k + S - 1 (fetched C - S iterations ago)
     cp_wait<S - 2>();
     __syncwarp();
-    // producer, part 1: the columns of position k + S - 1 (smem loads issued
-    // now, consumed after the consumer's work)
-    // positions k + S - 1 and k + C - 1: inside the consumer's chunk except
-    // in its last C - 1 iterations (chunks are >= C steps)
-    const bool inside = k + C - 1 < alen;
-    const int p = inside ? a0 + k + S - 1 : map(k + S - 1);
-    const int pcs = (int)((unsigned)(it + S - 1) % C);
-    bool issue = false;
-    int4 c0 = make_int4(0, 0, 0, 0), c1 = c0;
-    if (p >= 0) {
-      if (prem == 0) {  // header: no rows
-        prem = cr[pcs * SI + JPS];
-      } else {
-        --prem;
-        issue = true;
-        c0 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q];
-        c1 = reinterpret_cast<const int4*>(cr + pcs * SI)[2 * q + 1];
-      }
-    }
-    const int f = inside ? a0 + k + C - 1 : map(k + C - 1);
-#ifdef SELL_PF
-    {  // A steps are streamed once from HBM: pull position k + SELL_PF into L2
-      const int pf = map(k + SELL_PF);
-      if (pf >= 0 && lane < SI / 32)
-        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(steps + (size_t)pf * SI + lane * 32));
-    }
-#endif
+    const unsigned oth = HALF - hoff;
+    // producer, part 1: position k + S - 1 (slot u = 0: half h, S - 1; else the other half, u - 1)
+    const int* ps = reinterpret_cast<const int*>(s_sell + cro + (u == 0 ? hoff + (S - 1) * SI * 4 : oth + (u - 1) * SI * 4));
+    const bool pv = k + (S - 1) < alen + blen;
+    const int hv = ps[JPS];
+    const int4 c0 = reinterpret_cast<const int4*>(ps)[2 * q];
+    const int4 c1 = reinterpret_cast<const int4*>(ps)[2 * q + 1];
+    const bool issue = pv && prem != 0;
+    prem = pv ? (prem == 0 ? hv : prem - 1) : prem;
+    const int fv = k + (C - 1);
+    const bool fok = fv < alen + blen;
+    const int f = (fv < alen ? a0 : b0 - alen) + fv;  // real step (fok)
     // consumer: position k
-    const int* cw = cr + (int)((unsigned)it % C) * SI;
+    const int* cw = reinterpret_cast<const int*>(s_sell + cro + hoff + u * SI * 4);
     if (crem == 0) {  // header: finish the previous slice, start the next
+      if (k == alen) {  // the consumer leaves its chunk
+        resolve();
+        if (blen <= 0) {
+          nsteps += u;
+          return false;
+        }
+        a0 = b0;
+        alen = blen;
+        k = 0;
+        claim();
+        if (alen < S + C - 1) resolve();  // the last chunk may be short
+      }
       ++nslices;
-      epilogue((int)((unsigned)it % S));  // this position's row stage is free (a header gathers nothing)
+      epilogue(u);  // this position's row stage is free (a header gathers nothing)
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         out[g] = cw[g * 32 + lane];
@@ -462,15 +493,11 @@ seq_sell_kernel(const SellArgs a) {
       crem = cw[JPS];  // position 0 holds the slice's longest job
       t = 0;
     } else {
-      const unsigned char* xrow = wb + (int)((unsigned)it % S) * kSellStage;
+      const unsigned char* xrow = s_sell + u * kSellStage;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const float v = __int_as_float(cw[JPS + g * 32 + lane]);
-#ifdef SELL_NO_FP  // dev experiment (wrong results)
-        if (t < len[g] && v == 1234.5f) {
-#else
-        if (t < len[g]) {  // padding positions add nothing (also when X holds inf / NaN)
-#endif
+        if (!CHECK || t < len[g]) {  // padding adds nothing (also when X row 0 holds inf / NaN)
 #pragma unroll
           for (int c = 0; c < CPR; ++c) {
             const float4 x = *reinterpret_cast<const float4*>(xrow + roff[g][c]);
@@ -482,27 +509,41 @@ seq_sell_kernel(const SellArgs a) {
       ++t;
       --crem;
     }
-    // producer, part 2: rows of position k + S - 1 into the row slot, and the
-    // step of position k + C - 1 into the step slot, that position k - 1 used
-    if (issue) {
+    // producer, part 2: the rows of position k + S - 1, and the step of
+    // position k + C - 1 (slot u = 0: the other half, S - 1; else half h, u - 1)
+    {
       const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-      const unsigned d = xdst0 + (int)((unsigned)(it + S - 1) % S) * kSellStage;
+      const unsigned d = xdst0 + ((u + S - 1) % S) * kSellStage;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-#ifdef SELL_SKIP_HOT  // dev experiment: upper bound of a hot-row table (wrong results)
-        if (__popc(cc[i]) <= SELL_SKIP_HOT) continue;
-#endif
-#ifdef SELL_NO_GATHER  // dev experiment (wrong results)
-        if (cc[i] != -7) continue;
-#endif
-        cp16(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch));
+      for (int i = 0; i < 8; ++i) cp16_if(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch), issue);
+    }
+    {
+      const unsigned fs = smem_addr(s_sell) + cro + (u == 0 ? oth + (S - 1) * SI * 4 : hoff + (u - 1) * SI * 4);
+      const int* src = steps + (size_t)(unsigned)f * SI;  // not read unless fok
+      if constexpr (SI / 32 == 2) {
+        cp8_if(fs + lane * 8, src + lane * 2, fok);
+      } else {
+#pragma unroll
+        for (int o = 0; o < SI / 128; ++o) cp16_if(fs + (o * 32 + lane) * 16, src + (o * 32 + lane) * 4, fok);
       }
     }
-    fetch_step(f, (int)((unsigned)(it + C - 1) % C));
     cp_commit();
     ++k;
-    ++nsteps;
-  }
+    return true;
+  };
+  auto sweep = [&](auto chk) {
+#pragma unroll 1
+    for (;;) {
+      if (!bknown && k + (S + C - 2) >= alen) resolve();  // positions up to k + S + C - 2 this group
+      if (!SellUnroll<0, S>::run(step, chk)) return;
+      nsteps += S;
+      hoff = HALF - hoff;
+    }
+  };
+  if (row0_finite)
+    sweep(std::false_type{});
+  else
+    sweep(std::true_type{});
   cp_wait<0>();
   __syncwarp();
   epilogue(0);
