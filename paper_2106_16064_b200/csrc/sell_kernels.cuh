@@ -280,6 +280,7 @@ seq_sell_kernel(const SellArgs a) {
   const unsigned xr0 = smem_addr(wb);
   const unsigned cr0 = xr0 + S * kSellStage;
   const int col0 = blockIdx.y * CW;
+  const float x00 = a.K > 0 ? __ldg(a.X + col0 + lane % CW) : 0.f;  // X row 0 (padding rows), tested below
   const int* steps = a.steps;
   // LDGSTS lanes: group q = lane / LPR copies chunk lane % LPR of 8 rows, one
   // per instruction: rows 8 q + i at CW = 32 (4 rows 1 KB apart: 4 wavefronts,
@@ -432,8 +433,7 @@ seq_sell_kernel(const SellArgs a) {
   // Padding positions gather X row 0 and multiply it by 0: when this tile of
   // row 0 is finite that adds +-0 to an accumulator that is never -0 (same
   // bits), so the sweep runs without the per-job length test.
-  bool row0_finite = true;
-  if (a.K > 0) row0_finite = __all_sync(0xffffffffu, isfinite(__ldg(a.X + col0 + lane % CW)));
+  const bool row0_finite = __all_sync(0xffffffffu, isfinite(x00));
 
   // Main loop, in groups of S iterations (C = 2 S).  Iteration u of a group
   // consumes position k from step slot (half h, u) and row stage u, produces
@@ -466,6 +466,13 @@ seq_sell_kernel(const SellArgs a) {
     const int fv = k + (C - 1);
     const bool fok = fv < alen + blen;
     const int f = (fv < alen ? a0 : b0 - alen) + fv;  // real step (fok)
+    // producer, part 2: the rows of position k + S - 1 into row stage (u - 1) % S
+    auto gather = [&]() {
+      const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const unsigned d = xdst0 + ((u + S - 1) % S) * kSellStage;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cp16_if(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch), issue);
+    };
     // consumer: position k
     const int* cw = reinterpret_cast<const int*>(s_sell + cro + hoff + u * SI * 4);
     if (crem == 0) {  // header: finish the previous slice, start the next
@@ -492,31 +499,33 @@ seq_sell_kernel(const SellArgs a) {
       }
       crem = cw[JPS];  // position 0 holds the slice's longest job
       t = 0;
+      gather();
     } else {
+      // the row reads first, the gathers while they are in flight, then the math
       const unsigned char* xrow = s_sell + u * kSellStage;
+      float4 xs[G][CPR];
+      float vs[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float v = __int_as_float(cw[JPS + g * 32 + lane]);
+        vs[g] = __int_as_float(cw[JPS + g * 32 + lane]);
+#pragma unroll
+        for (int c = 0; c < CPR; ++c) xs[g][c] = *reinterpret_cast<const float4*>(xrow + roff[g][c]);
+      }
+      gather();
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
         if (!CHECK || t < len[g]) {  // padding adds nothing (also when X row 0 holds inf / NaN)
 #pragma unroll
           for (int c = 0; c < CPR; ++c) {
-            const float4 x = *reinterpret_cast<const float4*>(xrow + roff[g][c]);
-            f2_mac(acc[g][4 * c], acc[g][4 * c + 1], v, x.x, x.y, a.one2);
-            f2_mac(acc[g][4 * c + 2], acc[g][4 * c + 3], v, x.z, x.w, a.one2);
+            f2_mac(acc[g][4 * c], acc[g][4 * c + 1], vs[g], xs[g][c].x, xs[g][c].y, a.one2);
+            f2_mac(acc[g][4 * c + 2], acc[g][4 * c + 3], vs[g], xs[g][c].z, xs[g][c].w, a.one2);
           }
         }
       }
       ++t;
       --crem;
     }
-    // producer, part 2: the rows of position k + S - 1, and the step of
-    // position k + C - 1 (slot u = 0: the other half, S - 1; else half h, u - 1)
-    {
-      const int cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-      const unsigned d = xdst0 + ((u + S - 1) % S) * kSellStage;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cp16_if(d + i * ISTRIDE, xg + ((unsigned)cc[i] * n16 + ch), issue);
-    }
+    // and the step of position k + C - 1 (slot u = 0: the other half, S - 1; else half h, u - 1)
     {
       const unsigned fs = smem_addr(s_sell) + cro + (u == 0 ? oth + (S - 1) * SI * 4 : hoff + (u - 1) * SI * 4);
       const int* src = steps + (size_t)(unsigned)f * SI;  // not read unless fok
@@ -548,8 +557,8 @@ seq_sell_kernel(const SellArgs a) {
   __syncwarp();
   epilogue(0);
   if (lane == 0) {
-    // the last warp out resets the counters for the next call
-    __threadfence();
+    // the last warp out resets the counters for the next call (every claim of
+    // this warp has returned its value already: no fence needed before the count)
     if (atomicAdd(sched + 1, 1) == W - 1) {
       sched[0] = 0;
       sched[1] = 0;
