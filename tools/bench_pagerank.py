@@ -22,7 +22,10 @@ ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--l2", type=float, default=0.0, help="MB of x (its hot low-index prefix) pinned in L2")
 ap.add_argument("--kernel", default="rule", help="rule | tuned | par-rs | par-ws | seq-rs | seq-ws")
+ap.add_argument("--lib", default=None, help="dev: another build of libspmk_b200.so")
 args = ap.parse_args()
+if args.lib:
+    spmk.spmk.load_library(args.lib)
 t0 = time.time()
 d = spmk.DeviceCsr.generate_rmat(args.scale, args.ef, (0.57, 0.19, 0.19, 0.05), 1)
 torch.cuda.synchronize()

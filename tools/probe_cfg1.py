@@ -1,5 +1,8 @@
 import sys, json; sys.path.insert(0, ".")
 import torch, paper_2106_16064_b200 as spmk
+if len(sys.argv) > 1:
+    spmk.spmk.load_library(sys.argv[1])
+QUICK = len(sys.argv) > 2
 a = spmk.DeviceCsr.generate_rmat(16, 16, (0.25, 0.25, 0.25, 0.25), 1)
 x = spmk.make_dense_device(a.num_cols, 1, 0x00D5EED + 1)
 kid = a.select(1)
@@ -19,7 +22,12 @@ def graph_us(**tune):
         e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) * 1e3 / 100)
     return best
-for v in [dict(parws_impl=2, parws_cpt=0), dict(parws_impl=2, parws_cpt=1), dict(parws_impl=2, parws_cpt=2), dict(parws_impl=2, parws_cpt=4), dict(parws_impl=2, parws_cpt=8), dict(parws_impl=1, parws_t=4), dict(parws_impl=1, parws_t=8)]:
+if QUICK:
+    print(sys.argv[1], "par-ws", round(graph_us(), 2), "par-rs", end=" ")
+    kid = spmk.kParRowSplit
+    print(round(graph_us(), 2))
+    sys.exit(0)
+for v in [dict(parws_impl=2, parws_cpt=0), dict(parws_impl=2, parws_cpt=8), dict(parws_impl=2, parws_cpt=16), dict(parws_impl=2, parws_cpt=32), dict(parws_impl=2, parws_cpt=64), dict(parws_impl=1, parws_t=4)]:
     print(v, round(graph_us(**v), 2), flush=True)
 for k2 in spmk.kAllKernels:
     kid = k2
