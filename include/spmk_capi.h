@@ -230,10 +230,14 @@ spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes);
 /* Kernel launches issued by this library since load (all entry points). */
 uint64_t spmk_launch_count(void);
 /* When enabled, spmk_spmm records CUDA events on its stream around the
- * dominant (variant) kernel and around the whole call; spmk_timing_last
- * synchronizes on them and returns milliseconds.  For bench.py's roofline. */
+ * dominant (variant) kernel and around the whole call (one event set per call,
+ * the last 256 calls kept); spmk_timing_last synchronizes on the last call's
+ * events and returns milliseconds, spmk_timing_summary the totals over the
+ * calls kept since spmk_timing_enable (no host sync between the calls needed).
+ * For bench.py's roofline; no reference counterpart. */
 spmk_status spmk_timing_enable(int on);
 spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms);
+spmk_status spmk_timing_summary(float* main_kernel_ms, float* whole_call_ms, int* calls);
 /* Which device path spmk_spmm takes for (a, id, cfg, n) with 16-byte aligned
  * operands: *path = 1 for seq-ws through the lane-per-job sweep + fold pass
  * (sell_kernels.cuh; empty rows written in the sweep), 0 for the tile /

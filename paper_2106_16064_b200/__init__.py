@@ -28,6 +28,7 @@ from .spmk import (  # noqa: F401
     launch_count,
     timing_enable,
     timing_last,
+    timing_summary,
     load_library,
     make_dense_device,
     parse_kernel,

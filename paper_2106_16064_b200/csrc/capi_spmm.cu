@@ -15,10 +15,14 @@
 namespace spmk_host {
 namespace {
 
+// Event sets of the last kRing calls (one per call, reused cyclically), so a
+// caller can time many calls without synchronizing between them.
 struct Timing {
+  static constexpr int kRing = 256;
   bool on = false;
   int device = -1;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // call0, main0, main1, call1
+  long long calls = 0;  // calls recorded since enable
+  cudaEvent_t ev[kRing][4] = {};  // call0, main0, main1, call1
 };
 thread_local Timing g_timing;
 
@@ -27,12 +31,15 @@ void timing_record(int which, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_timing.device != dev) {
-    for (auto& e : g_timing.ev)
-      if (e) cudaEventDestroy(e);
-    for (auto& e : g_timing.ev) cudaEventCreate(&e);
+    for (auto& q : g_timing.ev)
+      for (auto& e : q) {
+        if (e) cudaEventDestroy(e);
+        cudaEventCreate(&e);
+      }
     g_timing.device = dev;
   }
-  cudaEventRecord(g_timing.ev[which], s);
+  if (which == 0) ++g_timing.calls;
+  cudaEventRecord(g_timing.ev[(g_timing.calls - 1) % Timing::kRing][which], s);
 }
 
 spmk_kernel_config cfg_or_default(const spmk_kernel_config* cfg) {
@@ -440,14 +447,36 @@ spmk_status spmk_l2_persist_x(void* stream, const float* d_x, size_t bytes) {
 
 spmk_status spmk_timing_enable(int on) {
   g_timing.on = on != 0;
+  g_timing.calls = 0;
   return SPMK_OK;
 }
 
 spmk_status spmk_timing_last(float* main_kernel_ms, float* whole_call_ms) {
-  if (!g_timing.on || !g_timing.ev[0]) return fail(SPMK_EINVAL, "timing not enabled / no call recorded");
-  if (cudaEventSynchronize(g_timing.ev[3]) != cudaSuccess) return fail(SPMK_ECUDA, "event sync");
-  if (main_kernel_ms) cudaEventElapsedTime(main_kernel_ms, g_timing.ev[1], g_timing.ev[2]);
-  if (whole_call_ms) cudaEventElapsedTime(whole_call_ms, g_timing.ev[0], g_timing.ev[3]);
+  if (!g_timing.on || g_timing.calls == 0) return fail(SPMK_EINVAL, "timing not enabled / no call recorded");
+  cudaEvent_t* q = g_timing.ev[(g_timing.calls - 1) % Timing::kRing];
+  if (cudaEventSynchronize(q[3]) != cudaSuccess) return fail(SPMK_ECUDA, "event sync");
+  if (main_kernel_ms) cudaEventElapsedTime(main_kernel_ms, q[1], q[2]);
+  if (whole_call_ms) cudaEventElapsedTime(whole_call_ms, q[0], q[3]);
+  return SPMK_OK;
+}
+
+spmk_status spmk_timing_summary(float* main_kernel_ms, float* whole_call_ms, int* calls) {
+  if (!g_timing.on || g_timing.calls == 0) return fail(SPMK_EINVAL, "timing not enabled / no call recorded");
+  const long long n = std::min<long long>(g_timing.calls, Timing::kRing);
+  if (cudaEventSynchronize(g_timing.ev[(g_timing.calls - 1) % Timing::kRing][3]) != cudaSuccess)
+    return fail(SPMK_ECUDA, "event sync");
+  double m = 0, w = 0;
+  for (long long i = g_timing.calls - n; i < g_timing.calls; ++i) {
+    cudaEvent_t* q = g_timing.ev[i % Timing::kRing];
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, q[1], q[2]);
+    cudaEventElapsedTime(&b, q[0], q[3]);
+    m += a;
+    w += b;
+  }
+  if (main_kernel_ms) *main_kernel_ms = (float)m;
+  if (whole_call_ms) *whole_call_ms = (float)w;
+  if (calls) *calls = (int)n;
   return SPMK_OK;
 }
 

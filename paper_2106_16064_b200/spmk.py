@@ -95,6 +95,7 @@ _SIGS = {
     "spmk_launch_count": ([], u64),
     "spmk_timing_enable": ([C.c_int], C.c_int),
     "spmk_timing_last": ([P(f32), P(f32)], C.c_int),
+    "spmk_timing_summary": ([P(f32), P(f32), P(C.c_int)], C.c_int),
     "spmk_mg_available": ([P(C.c_int)], C.c_int),
     "spmk_mg_unique_id": ([vp], C.c_int),
     "spmk_mg_init": ([vp, C.c_int, C.c_int, C.c_int, P(vp)], C.c_int),
@@ -539,3 +540,11 @@ def timing_last():
     a, b = f32(), f32()
     _check(load_library().spmk_timing_last(C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def timing_summary():
+    """(total dominant-kernel ms, total whole-call ms, calls) over the spmm calls
+    on this thread since timing_enable (the last 256 kept)."""
+    a, b, n = f32(), f32(), C.c_int()
+    _check(load_library().spmk_timing_summary(C.byref(a), C.byref(b), C.byref(n)))
+    return a.value, b.value, n.value
