@@ -110,6 +110,7 @@ struct SellPlan {
   int4* fold = nullptr;     // {row, first slot, slots} of the rows of >= 3 segments
   int nfold = 0;
   int nbig = 0;             // leading fold rows with > kFoldWarpMax slots (one CTA each)
+  int n4 = 0, n2 = 0;       // first fold rows with <= 4 / <= 2 slots (short-row tiers)
   long long nslots = 0;     // H slots (x N floats)
 };
 

@@ -214,11 +214,17 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStrea
     CK(cudaMemcpyAsync(ks.data(), key_s.p, sizeof(int) * p.nfold, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     while (p.nbig < p.nfold && ks[(size_t)p.nbig] > kFoldWarpMax) ++p.nbig;
+    p.n4 = p.nbig;
+    while (p.n4 < p.nfold && ks[(size_t)p.n4] > 4) ++p.n4;
+    p.n2 = p.n4;
+    while (p.n2 < p.nfold && ks[(size_t)p.n2] > 2) ++p.n2;
   } else if (p.nfold == 1) {
     int4 f1;
     CK(cudaMemcpyAsync(&f1, p.fold, sizeof(int4), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     p.nbig = f1.z > kFoldWarpMax ? 1 : 0;
+    p.n4 = f1.z > 4 ? 1 : 0;
+    p.n2 = f1.z > 2 ? 1 : 0;
   }
   if (h->nempty > 0) {
     sell_empty_jobs_kernel<<<grid_for(h->nempty), 256, 0, s>>>(h->erow, h->nempty, Jr, jstart.p, jlen.p, jout.p); LAUNCHED(1);
@@ -305,7 +311,12 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
   if (p.nfold > 0) {
     // programmatic dependent launch: scheduled while the sweep drains
     cudaLaunchConfig_t lc = {};
-    const long long small_warps = ((long long)(p.nfold - p.nbig) * tiles + kFoldRows - 1) / kFoldRows;
+    FoldTiers ft;
+    ft.n4 = p.n4;
+    ft.n2 = p.n2;
+    ft.w8 = (int)(((long long)(p.n4 - p.nbig) * tiles + 3) / 4);
+    ft.w4 = (int)(((long long)(p.n2 - p.n4) * tiles + 3) / 4);
+    const long long small_warps = (long long)ft.w8 + ft.w4 + ((long long)(p.nfold - p.n2) * tiles + 7) / 8;
     constexpr int wpb = kFoldThreads / 32;
     lc.gridDim = dim3((unsigned)((long long)p.nbig * tiles + (small_warps + wpb - 1) / wpb));
     lc.blockDim = dim3(kFoldThreads);
@@ -315,7 +326,7 @@ void launch_sell(spmk_csr_s* h, SellPlan& p, const float* X, int N, float* Y, fl
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&lc, sell_fold_kernel, (const int4*)p.fold, p.nfold, p.nbig, (const float*)H, Y, N)); LAUNCHED(1);
+    CK(cudaLaunchKernelEx(&lc, sell_fold_kernel, (const int4*)p.fold, p.nfold, p.nbig, ft, (const float*)H, Y, N)); LAUNCHED(1);
   }
 }
 

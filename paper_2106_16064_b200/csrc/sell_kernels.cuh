@@ -582,16 +582,56 @@ seq_sell_kernel(const SellArgs a) {
 //     one CTA per (row, tile) stages up to kFoldStage slots in shared memory
 //     with all its threads (every load in flight at once), then warp 0 adds
 //     them in order, lane = column;
-//   * the others (most rows: 2 slots): kFoldRows (row, tile) items per warp,
-//     all their loads in flight, lane = column.
+//   * the others (most rows: 2 slots): several (row, tile) items per warp by
+//     slot-count tier (below), all their loads in flight, lane = column.
 // Launched as a programmatic dependent of the sweep: the descriptor load
 // overlaps the sweep's tail, griddepcontrol.wait orders the H reads after it.
 constexpr int kFoldWarpMax = 8;
 constexpr int kFoldStage = 64;    // slots staged per round of a long row
-constexpr int kFoldRows = 4;      // short-row items per warp
 constexpr int kFoldThreads = 64;  // 2 warps per block: small blocks, many resident
+// Short rows (<= 8 slots) in three tiers of the slot-sorted fold list, each
+// warp taking R consecutive (row, tile) items with every load in flight:
+// 5..8 slots R = 4, 3..4 slots R = 4 (4 loads each), 2 slots R = 8 (most
+// split rows cross one boundary: 2 loads per item, none predicated off).
+struct FoldTiers {
+  int n4, n2;        // first fold row with <= 4 / <= 2 slots
+  int w8, w4;        // warps of the 5..8 and 3..4 tiers
+};
+// H is written by the sweep this kernel overlaps (programmatic dependent
+// launch): no __restrict__ on it, or its loads count as invariant and may be
+// hoisted above griddepcontrol.wait (seen: stale slots on a plan's first call).
+template <int R, int Z>
+__device__ __forceinline__ void fold_items(const int4* __restrict__ fold, int it0, int it_end, int tiles,
+                                           const float* H, float* __restrict__ Y, int N, int lane) {
+  int4 d[R];
+  int c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int it = it0 + r;
+    const int f = tiles == 1 ? it : it / tiles;
+    c[r] = (it - f * tiles) * 32 + lane;
+    d[r] = it < it_end && c[r] < N ? fold[f] : make_int4(0, 0, 0, 0);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  float v[R][Z];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float* h = H + (size_t)d[r].y * N + c[r];
+#pragma unroll
+    for (int u = 0; u < Z; ++u) v[r][u] = u < d[r].z ? h[(size_t)u * N] : 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (d[r].z == 0) continue;
+    float y = 0.f;
+#pragma unroll
+    for (int u = 0; u < Z; ++u)
+      if (u < d[r].z) y = __fadd_rn(y, v[r][u]);
+    st_y(Y + (size_t)d[r].x * N + c[r], y);
+  }
+}
 __global__ void __launch_bounds__(kFoldThreads, 16)
-sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float* __restrict__ H,
+sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, FoldTiers ft, const float* H,
                  float* __restrict__ Y, int N) {
   constexpr int WPB = kFoldThreads / 32;
   __shared__ float buf[kFoldStage][33];
@@ -634,36 +674,13 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, const float
     if (warp == 0 && colok) st_y(Y + (size_t)d.x * N + c0 + lane, y);
     return;
   }
-  // kFoldRows consecutive (row, tile) items per warp, all their loads in flight
-  const int item0 = nbig_items + (((int)blockIdx.x - nbig_items) * WPB + warp) * kFoldRows;
-  const int nitems = nfold * tiles;
-  int4 d[kFoldRows];
-  int c[kFoldRows];
-#pragma unroll
-  for (int r = 0; r < kFoldRows; ++r) {
-    const int it = item0 + r;
-    const int f = tiles == 1 ? it : it / tiles;
-    c[r] = (it - f * tiles) * 32 + lane;
-    d[r] = it < nitems && c[r] < N ? fold[f] : make_int4(0, 0, 0, 0);
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (item0 >= nitems) return;
-  float v[kFoldRows][kFoldWarpMax];
-#pragma unroll
-  for (int r = 0; r < kFoldRows; ++r) {
-    const float* h = H + (size_t)d[r].y * N + c[r];
-#pragma unroll
-    for (int u = 0; u < kFoldWarpMax; ++u) v[r][u] = u < d[r].z ? h[(size_t)u * N] : 0.f;
-  }
-#pragma unroll
-  for (int r = 0; r < kFoldRows; ++r) {
-    if (d[r].z == 0) continue;
-    float y = 0.f;
-#pragma unroll
-    for (int u = 0; u < kFoldWarpMax; ++u)
-      if (u < d[r].z) y = __fadd_rn(y, v[r][u]);
-    st_y(Y + (size_t)d[r].x * N + c[r], y);
-  }
+  const int gw = ((int)blockIdx.x - nbig_items) * WPB + warp;  // short-row warp
+  if (gw < ft.w8)
+    fold_items<4, 8>(fold, nbig_items + gw * 4, ft.n4 * tiles, tiles, H, Y, N, lane);
+  else if (gw < ft.w8 + ft.w4)
+    fold_items<4, 4>(fold, ft.n4 * tiles + (gw - ft.w8) * 4, ft.n2 * tiles, tiles, H, Y, N, lane);
+  else
+    fold_items<8, 2>(fold, ft.n2 * tiles + (gw - ft.w8 - ft.w4) * 8, nfold * tiles, tiles, H, Y, N, lane);
 }
 
 }  // namespace spmk_dev

@@ -200,3 +200,19 @@ def test_seq_rowsplit_through_the_sweep(orc, mixed, hub, n):
     torch.cuda.synchronize()
     d.set_tuning("hub_nnz", -1)
     same_bits(y.cpu().numpy(), orc.spmm(csr_of(a), 2, x))
+
+
+@pytest.mark.parametrize("n", [8, 32])
+def test_fold_reads_this_calls_partials(orc, n):
+    """The fold pass starts while the sweep drains (programmatic dependent
+    launch) and must read the H slots this call wrote: a fresh handle's first
+    call (H uninitialised) and then calls with other X (H holding the previous
+    call's partials) are all bit-exact."""
+    a = mixed_matrix(np.random.default_rng(11), m=2000)
+    d = spmk.DeviceCsr.from_host(a)
+    for chunk in (1, 7, 256):
+        cfg = spmk.KernelConfig(seq_chunk=chunk)
+        for seed in (1, 2, 3):
+            x = orc.make_dense(a.num_cols, n, 1000 * chunk + seed)
+            y = run(d, x, cfg, seq_impl=2)
+            same_bits(y, orc.spmm(csr_of(a), 3, x, seq_chunk=chunk))
