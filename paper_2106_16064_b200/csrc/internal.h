@@ -111,6 +111,7 @@ struct SellPlan {
   int nfold = 0;
   int nbig = 0;             // leading fold rows with > kFoldWarpMax slots (one CTA each)
   int n4 = 0, n2 = 0;       // first fold rows with <= 4 / <= 2 slots (short-row tiers)
+  int sms = 0;              // SMs of the device the plan was built for
   long long nslots = 0;     // H slots (x N floats)
 };
 

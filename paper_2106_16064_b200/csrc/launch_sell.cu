@@ -253,6 +253,7 @@ SellPlan& get_sell_plan(spmk_csr_s* h, long long CH, int lmax, int cw, cudaStrea
   int dev = 0, sms = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  p.sms = sms;
   p.blocks = sms * sell_blocks_per_sm(cw, shape);
   p.nwarps = p.blocks * kSellShapes[cw_index(cw)][shape].wpc;
   // Chunks of whole slices for the warps' work queue, guided sizes: about

@@ -587,7 +587,7 @@ seq_sell_kernel(const SellArgs a) {
 // Launched as a programmatic dependent of the sweep: the descriptor load
 // overlaps the sweep's tail, griddepcontrol.wait orders the H reads after it.
 constexpr int kFoldWarpMax = 8;
-constexpr int kFoldStage = 64;    // slots staged per round of a long row
+constexpr int kFoldStage = 96;    // slots staged per round of a long row (12.7 KB)
 constexpr int kFoldThreads = 64;  // 2 warps per block: small blocks, many resident
 // Short rows (<= 8 slots) in three tiers of the slot-sorted fold list, each
 // warp taking R consecutive (row, tile) items with every load in flight:
@@ -595,7 +595,7 @@ constexpr int kFoldThreads = 64;  // 2 warps per block: small blocks, many resid
 // split rows cross one boundary: 2 loads per item, none predicated off).
 struct FoldTiers {
   int n4, n2;        // first fold row with <= 4 / <= 2 slots
-  int w8, w4;        // warps of the 5..8 and 3..4 tiers
+  int w8, w4;        // work units of the 5..8 and 3..4 tiers
 };
 // H is written by the sweep this kernel overlaps (programmatic dependent
 // launch): no __restrict__ on it, or its loads count as invariant and may be
@@ -648,15 +648,15 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, FoldTiers f
     float y = 0.f;
     for (int k0 = 0; k0 < d.z; k0 += kFoldStage) {
       const int n = min(kFoldStage, d.z - k0);
-      // every load of the round in flight at once: slot r = warp + WPB u
-      float tmp[kFoldStage / WPB];
-#pragma unroll
-      for (int u = 0; u < kFoldStage / WPB; ++u) {
-        const int r = warp + WPB * u;
-        tmp[u] = r < n ? h[(size_t)(k0 + r) * N] : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < kFoldStage / WPB; ++u) buf[warp + WPB * u][lane] = tmp[u];
+      // every slot of the round in flight at once, straight into shared memory
+      // (4-byte cp.async: no register staging, so a round covers kFoldStage
+      // slots; cfg2: the rows of > 96 slots take two)
+      for (int r = warp; r < n; r += WPB)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(&buf[r][lane])),
+                     "l"(h + (size_t)(k0 + r) * N)
+                     : "memory");
+      cp_commit();
+      cp_wait<0>();
       __syncthreads();
       if (warp == 0) {
         int r = 0;
@@ -674,7 +674,9 @@ sell_fold_kernel(const int4* __restrict__ fold, int nfold, int nbig, FoldTiers f
     if (warp == 0 && colok) st_y(Y + (size_t)d.x * N + c0 + lane, y);
     return;
   }
-  const int gw = ((int)blockIdx.x - nbig_items) * WPB + warp;  // short-row warp
+  // one short-row work unit per warp (a grid-stride loop over fewer warps
+  // measured slower: 13-15 vs 9-11 us at cfg2)
+  const int gw = ((int)blockIdx.x - nbig_items) * WPB + warp;
   if (gw < ft.w8)
     fold_items<4, 8>(fold, nbig_items + gw * 4, ft.n4 * tiles, tiles, H, Y, N, lane);
   else if (gw < ft.w8 + ft.w4)
