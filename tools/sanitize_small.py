@@ -28,6 +28,9 @@ for skew in ((0.57, 0.19, 0.19, 0.05), (0.25, 0.25, 0.25, 0.25)):
                         d.set_tuning("sell_cfg", shape)
                         d.spmm(kid, x, cfg=cfg)
                     d.set_tuning("sell_cfg", 0)
+                    xi = x.clone()
+                    xi[0, 0] = float("inf")  # X row 0 not finite: the sweep's per-job length test
+                    d.spmm(kid, xi, cfg=cfg)
                     d.set_tuning("seq_impl", 3)
                     d.spmm(kid, x, cfg=cfg)
                     d.set_tuning("seq_impl", 2)
