@@ -588,7 +588,7 @@ seq_sell_kernel(const SellArgs a) {
 // overlaps the sweep's tail, griddepcontrol.wait orders the H reads after it.
 constexpr int kFoldWarpMax = 8;
 constexpr int kFoldStage = 96;    // slots staged per round of a long row (12.7 KB)
-constexpr int kFoldThreads = 64;  // 2 warps per block: small blocks, many resident
+constexpr int kFoldThreads = 64;  // 2 warps per block (measured: 128 the same, 32 slower)
 // Short rows (<= 8 slots) in three tiers of the slot-sorted fold list, each
 // warp taking R consecutive (row, tile) items with every load in flight:
 // 5..8 slots R = 4, 3..4 slots R = 4 (4 loads each), 2 slots R = 8 (most
