@@ -47,6 +47,7 @@ const Knob kKnobs[] = {
     {"l2_persist", "SPMK_L2_PERSIST", &Tuning::l2_persist},
     {"parws_impl", "SPMK_PARWS_IMPL", &Tuning::parws_impl},
     {"parws_cpt", "SPMK_PARWS_CPT", &Tuning::parws_cpt},
+    {"parws3", "SPMK_PARWS3", &Tuning::parws3},
     {"seq_impl", "SPMK_SEQ_IMPL", &Tuning::seq_impl},
     {"sell_cfg", "SPMK_SELL_CFG", &Tuning::sell_cfg},
 };

@@ -268,14 +268,30 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       const bool ws2 = W == 32 && N <= 2 && h->tune.parws_impl == 2;
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
-      long long cpt = h->tune.parws_cpt;
-      if (ws2 && cpt <= 0) {
-        const long long chunks = (h->nnz + 31) / 32;
-        cpt = 4;
-        while (cpt < 64 && chunks / (cpt * 2) >= 8LL * 148 * 32) cpt *= 2;
+      const long long chunks = (h->nnz + 31) / 32;
+      // SpMV: par_ws3 (no long rows) on tiles of ~chunks / 16K chunks (measured
+      // best on R-MAT uniform s16..s22: 4 .. 64); if the plan has long rows,
+      // par_ws2 on its own tiles (the largest power of two <= 64 that still
+      // gives >= 8 waves of 32 resident warps per SM)
+      bool ws3 = ws2 && N == 1 && h->tune.parws3 != 0;
+      auto ws_cpt = [&](bool three) {
+        long long c = h->tune.parws_cpt;
+        if (c > 0) return c;
+        c = 4;
+        if (three)
+          while (c < 64 && chunks > 16384LL * c) c *= 2;
+        else
+          while (c < 64 && chunks / (c * 2) >= 8LL * 148 * 32) c *= 2;
+        return c;
+      };
+      long long TS = ws2 ? CH * ws_cpt(ws3) : CH * T;
+      Plan* pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
+      if (ws3 && pp->nlong > 0) {
+        ws3 = false;
+        TS = CH * ws_cpt(false);
+        pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
       }
-      const long long TS = ws2 ? CH * cpt : CH * T;
-      Plan& p = get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
+      Plan& p = *pp;
       a.rlo = p.rlo;
       a.desc = p.desc;
       a.TS = TS;
@@ -288,7 +304,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       }
       const unsigned* hf = ws2 ? get_head_flags32(h, s) : nullptr;
       timing_record(1, s);
-      if (ws2) launch_par_ws2(a, hf, aligned, s);
+      if (ws3) launch_par_ws3(a, hf, h->mne == h->m, s);
+      else if (ws2) launch_par_ws2(a, hf, aligned, s);
       else launch_par_ws(a, W, T, aligned, s);
       timing_record(2, s);
       if (p.nlong > 0) launch_fixup(p, a.H, a.Tsl, d_y, N, s);

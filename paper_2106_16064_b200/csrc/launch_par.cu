@@ -14,6 +14,7 @@
 #include "par_ws.cuh"
 #include "par_ws64.cuh"
 #include "par_ws2.cuh"
+#include "par_ws3.cuh"
 
 using namespace spmk_dev;
 
@@ -202,6 +203,12 @@ void launch_par_ws2(const ParLaunch& l, const unsigned* hflag, bool aligned, cud
   if (ct == 1) par_ws2_kernel<1, 2><<<grid, 256, 0, s>>>(A);
   else par_ws2_kernel<2, 2><<<grid, 256, 0, s>>>(A);
   LAUNCHED(1);
+}
+
+void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, cudaStream_t s) {
+  ParWs2Args A{to_args(l), hflag};
+  if (rid_ident) A.p.rid = nullptr;  // no empty rows: compact row r is row r
+  par_ws3_kernel<<<(unsigned)((A.p.nunits + 7) / 8), 256, 0, s>>>(A); LAUNCHED(1);
 }
 
 void launch_par_ws64(const ParLaunch& l, float* slots, cudaStream_t s) {
