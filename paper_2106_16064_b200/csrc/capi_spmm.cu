@@ -269,11 +269,11 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
       const long long chunks = (h->nnz + 31) / 32;
-      // SpMV: par_ws3 (no long rows) on tiles of ~chunks / 16K chunks (measured
+      // N <= 2: par_ws3 (no long rows) on tiles of ~chunks / 16K chunks (measured
       // best on R-MAT uniform s16..s22: 4 .. 64); if the plan has long rows,
       // par_ws2 on its own tiles (the largest power of two <= 64 that still
       // gives >= 8 waves of 32 resident warps per SM)
-      bool ws3 = ws2 && N == 1 && h->tune.parws3 != 0;
+      bool ws3 = ws2 && h->tune.parws3 != 0;
       auto ws_cpt = [&](bool three) {
         long long c = h->tune.parws_cpt;
         if (c > 0) return c;
@@ -304,7 +304,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       }
       const unsigned* hf = ws2 ? get_head_flags32(h, s) : nullptr;
       timing_record(1, s);
-      if (ws3) launch_par_ws3(a, hf, h->mne == h->m, s);
+      if (ws3) launch_par_ws3(a, hf, h->mne == h->m, aligned, s);
       else if (ws2) launch_par_ws2(a, hf, aligned, s);
       else launch_par_ws(a, W, T, aligned, s);
       timing_record(2, s);

@@ -205,10 +205,14 @@ void launch_par_ws2(const ParLaunch& l, const unsigned* hflag, bool aligned, cud
   LAUNCHED(1);
 }
 
-void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, cudaStream_t s) {
+void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, bool aligned, cudaStream_t s) {
   ParWs2Args A{to_args(l), hflag};
   if (rid_ident) A.p.rid = nullptr;  // no empty rows: compact row r is row r
-  par_ws3_kernel<<<(unsigned)((A.p.nunits + 7) / 8), 256, 0, s>>>(A); LAUNCHED(1);
+  A.p.xvec = aligned ? 1 : 0;
+  const unsigned grid = (unsigned)((A.p.nunits + 7) / 8);
+  if (A.p.N == 1) par_ws3_kernel<1><<<grid, 256, 0, s>>>(A);
+  else par_ws3_kernel<2><<<grid, 256, 0, s>>>(A);
+  LAUNCHED(1);
 }
 
 void launch_par_ws64(const ParLaunch& l, float* slots, cudaStream_t s) {

@@ -1,4 +1,4 @@
-// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for SpMV (N = 1) on
+// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for N = 1 / 2 on
 // matrices without long rows: the par_ws2 sweep with one chunk per
 // iteration and only the arithmetic that case needs.
 //
@@ -25,6 +25,26 @@
 
 namespace spmk_dev {
 
+// dense row of CT columns at column index c (CT = 2: one 8-byte load when X
+// is 8-byte aligned)
+template <int CT>
+__device__ __forceinline__ void ws3_gather(const float* X, int c, bool vec, float (&x)[CT]) {
+  const float* r = X + (size_t)(unsigned)c * CT;
+  if constexpr (CT == 1) {
+    x[0] = ld_x(r);
+  } else {
+    if (vec) {
+      const float2 t = ld_x2(r);
+      x[0] = t.x;
+      x[1] = t.y;
+    } else {
+      x[0] = ld_x(r);
+      x[1] = ld_x(r + 1);
+    }
+  }
+}
+
+template <int CT>
 __global__ void __launch_bounds__(256)
 par_ws3_kernel(const ParWs2Args A) {
   constexpr unsigned FULL = 0xffffffffu;
@@ -45,6 +65,7 @@ par_ws3_kernel(const ParWs2Args A) {
   const int q_end = (hard_end + 31) >> 5;  // exclusive
   const int* const rid = a.rid;
   const int rmax = a.mne - 1;
+  const bool vec = a.xvec != 0;
 
   // chunk q's colIdx / val / head word, zero outside [lo, hard_end)
   auto load_cv = [&](int q, int& c, float& v, unsigned& m) {
@@ -58,24 +79,26 @@ par_ws3_kernel(const ParWs2Args A) {
   auto row_of = [&](int cr, unsigned M) { return cr + __popc(M & le & ~1u); };
 
   // pipeline: chunk q computing, q + 1 gathered, q + 2 loading
-  int c1, c2;
-  float v0, v1, v2, x0;
+  int c0, c1, c2;
+  float v0, v1, v2, x0[CT];
   unsigned m0, m1, m2;
-  int c0;
   load_cv(q_beg, c0, v0, m0);
   load_cv(q_beg + 1, c1, v1, m1);
   load_cv(q_beg + 2, c2, v2, m2);
-  x0 = ld_x(a.X + (size_t)(unsigned)c0);
-  // row-end row ids of chunk q (prefetched a chunk ahead)
+  ws3_gather<CT>(a.X, c0, vec, x0);
+  // row-end row ids of chunk q (looked up a chunk ahead)
   int rid0 = 0;
   if (rid) rid0 = rid[min(row_of(cur, m0), rmax)];
-  float carry = 0.f;
+  float carry[CT];
+#pragma unroll
+  for (int j = 0; j < CT; ++j) carry[j] = 0.f;
   bool has_carry = false;
 
 #pragma unroll 1
   for (int q = q_beg; q < q_end; ++q) {
     // gather chunk q + 1, look up its row ids, load chunk q + 3
-    const float x1 = ld_x(a.X + (size_t)(unsigned)c1);
+    float x1[CT];
+    ws3_gather<CT>(a.X, c1, vec, x1);
     const int cur1 = cur + __popc(m0 & ~1u) + (int)(m1 & 1u);  // compact row containing 32(q+1)
     int rid1 = 0;
     if (rid) rid1 = rid[min(row_of(cur1, m1), rmax)];
@@ -88,38 +111,60 @@ par_ws3_kernel(const ParWs2Args A) {
     const int cq = q << 5;
     const int p = cq + lane;
     const bool live = p >= lo && p < hard_end;
-    float v = __fmul_rn(v0, x0);  // kernels.hpp:277 (dead lanes: val 0, never read by live runs)
+    float v[CT];
+#pragma unroll
+    for (int j = 0; j < CT; ++j) v[j] = __fmul_rn(v0, x0[j]);  // kernels.hpp:277 (dead lanes: never read by live runs)
     const unsigned mle = m0 & le;
     const int sst = max(31 - __clz(mle), 0);  // first lane of this lane's run in the chunk
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {  // reduction.hpp:77-85, lockstep
-      const float up = __shfl_up_sync(FULL, v, off);
-      if (lane - off >= sst) v = __fadd_rn(v, up);
+      const bool same = lane - off >= sst;
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const float up = __shfl_up_sync(FULL, v[j], off);
+        if (same) v[j] = __fadd_rn(v[j], up);
+      }
     }
     const unsigned nh = __funnelshift_r(m0, m1, 1);  // bit l: position 32q + l + 1 starts a row
-    const bool first_run = mle == 0;                 // run open since before this chunk
-    const float t = (first_run && has_carry) ? __fadd_rn(carry, v) : v;
+    const bool add_carry = mle == 0 && has_carry;    // run open since before this chunk
+    float t[CT];
+#pragma unroll
+    for (int j = 0; j < CT; ++j) t[j] = add_carry ? __fadd_rn(carry[j], v[j]) : v[j];
     if (live && ((nh >> lane) & 1u)) {
       const int row = rid ? rid0 : row_of(cur, m0);
-      st_y(a.Y + (size_t)(unsigned)row, t);
+      float* y = a.Y + (size_t)(unsigned)row * CT;
+      if constexpr (CT == 1) {
+        st_y(y, t[0]);
+      } else if (vec) {  // X and Y 16-byte aligned: rows of 2 floats are 8-byte aligned
+        st_y2(y, t[0], t[1]);
+      } else {
+        st_y(y, t[0]);
+        st_y(y + 1, t[1]);
+      }
     }
     // the run crossing the chunk's last live lane (if any) becomes the carry
     const int ll = min(hard_end - cq, 32) - 1;
-    const float tl = __shfl_sync(FULL, t, ll);
+    float tl[CT];
+#pragma unroll
+    for (int j = 0; j < CT; ++j) tl[j] = __shfl_sync(FULL, t[j], ll);
     if (!((nh >> ll) & 1u)) {
       const unsigned le_ll = (ll == 31) ? FULL : ((2u << ll) - 1u);
       if ((m0 & le_ll) != 0) {  // a run starting in this chunk
-        carry = __fadd_rn(0.f, tl);  // Y starts at +0
+#pragma unroll
+        for (int j = 0; j < CT; ++j) carry[j] = __fadd_rn(0.f, tl[j]);  // Y starts at +0
         has_carry = true;
       } else {
-        carry = tl;
+#pragma unroll
+        for (int j = 0; j < CT; ++j) carry[j] = tl[j];
       }
     } else {
       has_carry = false;
     }
     cur = cur1;
     // rotate
-    c0 = c1; v0 = v1; m0 = m1; x0 = x1; rid0 = rid1;
+    c0 = c1; v0 = v1; m0 = m1; rid0 = rid1;
+#pragma unroll
+    for (int j = 0; j < CT; ++j) x0[j] = x1[j];
     c1 = c2; v1 = v2; m1 = m2;
     c2 = c3; v2 = v3; m2 = m3;
   }
