@@ -269,11 +269,11 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
       const long long chunks = (h->nnz + 31) / 32;
-      // N <= 2: par_ws3 (no long rows) on tiles of ~chunks / 16K chunks (measured
-      // best on R-MAT uniform s16..s22: 4 .. 64); if the plan has long rows,
-      // par_ws2 on its own tiles (the largest power of two <= 64 that still
-      // gives >= 8 waves of 32 resident warps per SM)
-      bool ws3 = ws2 && h->tune.parws3 != 0;
+      // N = 1 / 2 / 4: par_ws3 (plans without long rows) on tiles of ~chunks /
+      // 16K chunks (measured best on R-MAT uniform s16..s22: 4 .. 64); with long
+      // rows, par_ws2 (N <= 2) on its own tiles (the largest power of two <= 64
+      // that still gives >= 8 waves of 32 resident warps per SM) or the tile kernel
+      bool ws3 = W == 32 && (N <= 2 || N == 4) && h->tune.parws_impl == 2 && h->tune.parws3 != 0;
       auto ws_cpt = [&](bool three) {
         long long c = h->tune.parws_cpt;
         if (c > 0) return c;
@@ -284,11 +284,11 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
           while (c < 64 && chunks / (c * 2) >= 8LL * 148 * 32) c *= 2;
         return c;
       };
-      long long TS = ws2 ? CH * ws_cpt(ws3) : CH * T;
+      long long TS = ws3 ? CH * ws_cpt(true) : (ws2 ? CH * ws_cpt(false) : CH * T);
       Plan* pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
       if (ws3 && pp->nlong > 0) {
         ws3 = false;
-        TS = CH * ws_cpt(false);
+        TS = ws2 ? CH * ws_cpt(false) : CH * T;
         pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
       }
       Plan& p = *pp;
@@ -302,7 +302,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         a.H = sc;
         a.Tsl = sc + (size_t)nch * N;
       }
-      const unsigned* hf = ws2 ? get_head_flags32(h, s) : nullptr;
+      const unsigned* hf = ws2 || ws3 ? get_head_flags32(h, s) : nullptr;
       timing_record(1, s);
       if (ws3) launch_par_ws3(a, hf, h->mne == h->m, aligned, s);
       else if (ws2) launch_par_ws2(a, hf, aligned, s);

@@ -264,7 +264,7 @@ void launch_par_rs(const ParLaunch& a, int W, int vl, bool aligned, cudaStream_t
 void launch_par_ws(const ParLaunch& a, int W, int T, bool aligned, cudaStream_t s);
 void launch_par_ws64(const ParLaunch& a, float* slots, cudaStream_t s);  // lane_width 64
 void launch_par_ws2(const ParLaunch& a, const unsigned* hflag, bool aligned, cudaStream_t s);
-// W 32, N = 1 / 2, plan without long rows; rid_ident: no empty rows
+// W 32, N = 1 / 2 / 4, plan without long rows; rid_ident: no empty rows
 void launch_par_ws3(const ParLaunch& a, const unsigned* hflag, bool rid_ident, bool aligned, cudaStream_t s);  // W 32, N <= 2
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, int L, const float* d_x, int N,
                  float* d_y, cudaStream_t s);

@@ -211,7 +211,8 @@ void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, b
   A.p.xvec = aligned ? 1 : 0;
   const unsigned grid = (unsigned)((A.p.nunits + 7) / 8);
   if (A.p.N == 1) par_ws3_kernel<1><<<grid, 256, 0, s>>>(A);
-  else par_ws3_kernel<2><<<grid, 256, 0, s>>>(A);
+  else if (A.p.N == 2) par_ws3_kernel<2><<<grid, 256, 0, s>>>(A);
+  else par_ws3_kernel<4><<<grid, 256, 0, s>>>(A);
   LAUNCHED(1);
 }
 

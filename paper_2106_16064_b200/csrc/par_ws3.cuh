@@ -1,4 +1,4 @@
-// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for N = 1 / 2 on
+// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for N = 1 / 2 / 4 on
 // matrices without long rows: the par_ws2 sweep with one chunk per
 // iteration and only the arithmetic that case needs.
 //
@@ -25,14 +25,14 @@
 
 namespace spmk_dev {
 
-// dense row of CT columns at column index c (CT = 2: one 8-byte load when X
-// is 8-byte aligned)
+// dense row of CT columns at column index c (CT = 2 / 4: one 8- / 16-byte
+// load when X is 16-byte aligned)
 template <int CT>
 __device__ __forceinline__ void ws3_gather(const float* X, int c, bool vec, float (&x)[CT]) {
   const float* r = X + (size_t)(unsigned)c * CT;
   if constexpr (CT == 1) {
     x[0] = ld_x(r);
-  } else {
+  } else if constexpr (CT == 2) {
     if (vec) {
       const float2 t = ld_x2(r);
       x[0] = t.x;
@@ -40,6 +40,17 @@ __device__ __forceinline__ void ws3_gather(const float* X, int c, bool vec, floa
     } else {
       x[0] = ld_x(r);
       x[1] = ld_x(r + 1);
+    }
+  } else {
+    if (vec) {
+      const float4 t = ld_x4(r);
+      x[0] = t.x;
+      x[1] = t.y;
+      x[2] = t.z;
+      x[3] = t.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < CT; ++j) x[j] = ld_x(r + j);
     }
   }
 }
@@ -135,11 +146,12 @@ par_ws3_kernel(const ParWs2Args A) {
       float* y = a.Y + (size_t)(unsigned)row * CT;
       if constexpr (CT == 1) {
         st_y(y, t[0]);
-      } else if (vec) {  // X and Y 16-byte aligned: rows of 2 floats are 8-byte aligned
-        st_y2(y, t[0], t[1]);
+      } else if (vec) {  // X and Y 16-byte aligned: rows of CT floats are 4 CT-byte aligned
+        if constexpr (CT == 2) st_y2(y, t[0], t[1]);
+        else st_y4(y, t[0], t[1], t[2], t[3]);
       } else {
-        st_y(y, t[0]);
-        st_y(y + 1, t[1]);
+#pragma unroll
+        for (int j = 0; j < CT; ++j) st_y(y + j, t[j]);
       }
     }
     // the run crossing the chunk's last live lane (if any) becomes the carry

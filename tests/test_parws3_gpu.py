@@ -46,7 +46,7 @@ def same_bits(y, want):
     assert np.array_equal(y[~yn].view(np.uint32), want[~wn].view(np.uint32))
 
 
-@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("n", [1, 2, 4])
 @pytest.mark.parametrize("empty_rows", [False, True])
 @pytest.mark.parametrize("cpt", [0, 4, 8, 64])
 def test_bit_exact(orc, empty_rows, cpt, n):
@@ -68,7 +68,7 @@ def test_bit_exact(orc, empty_rows, cpt, n):
         assert np.all(y[e] == 0) and not np.any(np.signbit(y[e]))
 
 
-@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("n", [1, 2, 4])
 def test_long_rows_fall_back(orc, n):
     """A row longer than a tile makes the plan carry long rows: the call takes
     par_ws2 (H / T partials + fix-up) and stays bit-exact."""
@@ -82,7 +82,7 @@ def test_long_rows_fall_back(orc, n):
     same_bits(run(d, x, parws3=1, parws_cpt=4), orc.spmm(csr_of(a), 1, x))
 
 
-@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("n", [1, 2, 4])
 def test_inf_nan_in_x(orc, n):
     """Dead lanes gather X row 0 and live runs never read them: inf / NaN in
     X (row 0 too) give the reference's bits."""
@@ -97,19 +97,20 @@ def test_inf_nan_in_x(orc, n):
     same_bits(run(d, x, parws3=1, parws_cpt=0), orc.spmm(csr_of(a), 1, x))
 
 
-def test_unaligned_operands(orc):
-    """N = 2 with X / Y views 4 bytes off a 16-byte boundary: scalar loads and
-    stores, same bits."""
+@pytest.mark.parametrize("n", [2, 4])
+def test_unaligned_operands(orc, n):
+    """X / Y views 4 bytes off a 16-byte boundary: scalar loads and stores,
+    same bits."""
     rng = np.random.default_rng(2)
     m, k = 1500, 1200
     a = rows_matrix(rng, m, k, rng.integers(1, 40, m))
     d = spmk.DeviceCsr.from_host(a)
-    x = orc.make_dense(k, 2, 31)
+    x = orc.make_dense(k, n, 31)
     d.set_tuning("parws3", 1)
     d.set_tuning("parws_cpt", 0)
-    xb = torch.zeros(k * 2 + 1, device="cuda")
+    xb = torch.zeros(k * n + 1, device="cuda")
     xb[1:] = torch.from_numpy(x).cuda().view(-1)
-    yb = torch.full((m * 2 + 1,), float("nan"), device="cuda")
-    d.spmm(spmk.kParBalanced, xb[1:].view(k, 2), yb[1:].view(m, 2))
+    yb = torch.full((m * n + 1,), float("nan"), device="cuda")
+    d.spmm(spmk.kParBalanced, xb[1:].view(k, n), yb[1:].view(m, n))
     torch.cuda.synchronize()
-    same_bits(yb[1:].view(m, 2).cpu().numpy(), orc.spmm(csr_of(a), 1, x))
+    same_bits(yb[1:].view(m, n).cpu().numpy(), orc.spmm(csr_of(a), 1, x))
