@@ -286,7 +286,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       };
       long long TS = ws3 ? CH * ws_cpt(true) : (ws2 ? CH * ws_cpt(false) : CH * T);
       Plan* pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
-      if (ws3 && pp->nlong > 0) {
+      if (ws3 && pp->nlong > 0 && h->tune.parws3 < 2) {
         ws3 = false;
         TS = ws2 ? CH * ws_cpt(false) : CH * T;
         pp = &get_plan(h, 2, TS, CH, h->tune.parws_ext, s);
@@ -304,7 +304,7 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       }
       const unsigned* hf = ws2 || ws3 ? get_head_flags32(h, s) : nullptr;
       timing_record(1, s);
-      if (ws3) launch_par_ws3(a, hf, h->mne == h->m, aligned, s);
+      if (ws3) launch_par_ws3(a, hf, h->mne == h->m, aligned, p.nlong > 0, s);
       else if (ws2) launch_par_ws2(a, hf, aligned, s);
       else launch_par_ws(a, W, T, aligned, s);
       timing_record(2, s);

@@ -205,15 +205,21 @@ void launch_par_ws2(const ParLaunch& l, const unsigned* hflag, bool aligned, cud
   LAUNCHED(1);
 }
 
-void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, bool aligned, cudaStream_t s) {
+template <bool LONG>
+void launch_par_ws3_t(const ParWs2Args& A, cudaStream_t s) {
+  const unsigned grid = (unsigned)((A.p.nunits + 7) / 8);
+  if (A.p.N == 1) par_ws3_kernel<1, LONG><<<grid, 256, 0, s>>>(A);
+  else if (A.p.N == 2) par_ws3_kernel<2, LONG><<<grid, 256, 0, s>>>(A);
+  else par_ws3_kernel<4, LONG><<<grid, 256, 0, s>>>(A);
+  LAUNCHED(1);
+}
+void launch_par_ws3(const ParLaunch& l, const unsigned* hflag, bool rid_ident, bool aligned, bool long_rows,
+                    cudaStream_t s) {
   ParWs2Args A{to_args(l), hflag};
   if (rid_ident) A.p.rid = nullptr;  // no empty rows: compact row r is row r
   A.p.xvec = aligned ? 1 : 0;
-  const unsigned grid = (unsigned)((A.p.nunits + 7) / 8);
-  if (A.p.N == 1) par_ws3_kernel<1><<<grid, 256, 0, s>>>(A);
-  else if (A.p.N == 2) par_ws3_kernel<2><<<grid, 256, 0, s>>>(A);
-  else par_ws3_kernel<4><<<grid, 256, 0, s>>>(A);
-  LAUNCHED(1);
+  if (long_rows) launch_par_ws3_t<true>(A, s);
+  else launch_par_ws3_t<false>(A, s);
 }
 
 void launch_par_ws64(const ParLaunch& l, float* slots, cudaStream_t s) {

@@ -55,7 +55,7 @@ __device__ __forceinline__ void ws3_gather(const float* X, int c, bool vec, floa
   }
 }
 
-template <int CT>
+template <int CT, bool LONG>
 __global__ void __launch_bounds__(256)
 par_ws3_kernel(const ParWs2Args A) {
   constexpr unsigned FULL = 0xffffffffu;
@@ -66,12 +66,16 @@ par_ws3_kernel(const ParWs2Args A) {
   const uint64_t pol = evict_first_policy();
   const unsigned le = (lane == 31) ? FULL : ((2u << lane) - 1u);
   const int4 dsc = a.desc[unit];
-  const int lo = dsc.y;        // first live position (a row head)
+  const int lo = dsc.y;        // first live position (a row head, or the tile start inside a long row)
   const int hard_end = dsc.z;  // end of the last row this tile owns
   if (lo >= hard_end) return;
+  // LONG (plans with long rows): the row entering the tile may be long; its
+  // per-chunk partials go to H, an owner's prefix of a long row crossing the
+  // tile end to T (fixup_kernel merges them), as in par_ws2
+  int mode = LONG ? dsc.w : MODE_NORMAL;
   // compact row containing the first swept chunk's first position
   int cur = dsc.x;
-  if ((lo & 31) != 0) cur = dsc.x - 1;  // lanes before lo: row r-1 (dead)
+  if (mode == MODE_NORMAL && (lo & 31) != 0) cur = dsc.x - 1;  // lanes before lo: row r-1 (dead)
   const int q_beg = lo >> 5;
   const int q_end = (hard_end + 31) >> 5;  // exclusive
   const int* const rid = a.rid;
@@ -103,7 +107,7 @@ par_ws3_kernel(const ParWs2Args A) {
   float carry[CT];
 #pragma unroll
   for (int j = 0; j < CT; ++j) carry[j] = 0.f;
-  bool has_carry = false;
+  bool has_carry = LONG && mode == MODE_ENTER_LONG;
 
 #pragma unroll 1
   for (int q = q_beg; q < q_end; ++q) {
@@ -137,11 +141,19 @@ par_ws3_kernel(const ParWs2Args A) {
       }
     }
     const unsigned nh = __funnelshift_r(m0, m1, 1);  // bit l: position 32q + l + 1 starts a row
-    const bool add_carry = mle == 0 && has_carry;    // run open since before this chunk
+    const bool first_run = mle == 0;                 // run open since before this chunk
+    const bool add_carry = first_run && has_carry && (!LONG || mode == MODE_NORMAL);
     float t[CT];
 #pragma unroll
     for (int j = 0; j < CT; ++j) t[j] = add_carry ? __fadd_rn(carry[j], v[j]) : v[j];
-    if (live && ((nh >> lane) & 1u)) {
+    if (LONG && first_run && mode == MODE_ENTER_LONG) {
+      // long row: this chunk's partial from its last lane in the chunk
+      if (live && (((nh >> lane) & 1u) || p + 1 == min(cq + 32, hard_end))) {
+        float* h = a.H + (size_t)q * CT;
+#pragma unroll
+        for (int j = 0; j < CT; ++j) h[j] = t[j];
+      }
+    } else if (live && ((nh >> lane) & 1u)) {
       const int row = rid ? rid0 : row_of(cur, m0);
       float* y = a.Y + (size_t)(unsigned)row * CT;
       if constexpr (CT == 1) {
@@ -165,12 +177,14 @@ par_ws3_kernel(const ParWs2Args A) {
 #pragma unroll
         for (int j = 0; j < CT; ++j) carry[j] = __fadd_rn(0.f, tl[j]);  // Y starts at +0
         has_carry = true;
-      } else {
+        mode = MODE_NORMAL;
+      } else if (!LONG || mode == MODE_NORMAL) {
 #pragma unroll
         for (int j = 0; j < CT; ++j) carry[j] = tl[j];
       }
     } else {
       has_carry = false;
+      mode = MODE_NORMAL;
     }
     cur = cur1;
     // rotate
@@ -179,6 +193,14 @@ par_ws3_kernel(const ParWs2Args A) {
     for (int j = 0; j < CT; ++j) x0[j] = x1[j];
     c1 = c2; v1 = v2; m1 = m2;
     c2 = c3; v2 = v3; m2 = m3;
+  }
+  if constexpr (LONG) {
+    // long row crossing the tile end (its owner does not extend): prefix -> T slot
+    const int te = min(unit * (int)a.TS + (int)a.TS, a.nnz);
+    if (hard_end == te && te < a.nnz && has_carry && mode == MODE_NORMAL && lane == 0) {
+#pragma unroll
+      for (int j = 0; j < CT; ++j) a.Tsl[(size_t)unit * CT + j] = carry[j];
+    }
   }
 }
 

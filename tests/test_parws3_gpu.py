@@ -69,17 +69,23 @@ def test_bit_exact(orc, empty_rows, cpt, n):
 
 
 @pytest.mark.parametrize("n", [1, 2, 4])
-def test_long_rows_fall_back(orc, n):
-    """A row longer than a tile makes the plan carry long rows: the call takes
-    par_ws2 (H / T partials + fix-up) and stays bit-exact."""
+def test_long_rows(orc, n):
+    """Rows longer than a tile make the plan carry long rows (per-chunk H
+    partials, owner prefixes in T, fix-up): bit-exact through par_ws3's long
+    mode and through par_ws2 / the tile kernel."""
     rng = np.random.default_rng(9)
     m, k = 3000, 9000
     lens = rng.integers(0, 40, m)
     lens[7] = 8000
+    lens[100] = 700
+    lens[101] = 300
     a = rows_matrix(rng, m, k, lens)
     d = spmk.DeviceCsr.from_host(a)
     x = orc.make_dense(k, n, 4)
-    same_bits(run(d, x, parws3=1, parws_cpt=4), orc.spmm(csr_of(a), 1, x))
+    want = orc.spmm(csr_of(a), 1, x)
+    for cpt in (4, 8, 0):
+        same_bits(run(d, x, parws3=1, parws_cpt=cpt), want)  # par_ws2 / tile kernel
+        same_bits(run(d, x, parws3=2, parws_cpt=cpt), want)  # par_ws3 with H / T partials
 
 
 @pytest.mark.parametrize("n", [1, 2, 4])
