@@ -259,21 +259,18 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       launch_par_ws64(a, slots, s);
       timing_record(2, s);
     } else {
-      // W = 32, N <= 2 (SpMV: cfg1, cfg5, PageRank): the streaming head-flag
-      // kernel, tiles of C chunks (the largest power of two <= 64 that still
-      // gives >= 8 waves of 32 resident warps per SM: small tail);
-      // otherwise T chunks of W nonzeros per tile (4 or 8: the two compiled shapes)
-      // (measured on B200: N = 1 / 2 / 4 on R-MAT s20 122 / 131 / 175 us vs
-      // 124 / 139 / 166 us for the tile kernel; cfg5 SpMV 2.72 vs 3.62 ms)
+      // W = 32, N <= 4: par_ws3 (below); with parws3 = 0, N <= 2 the streaming
+      // head-flag kernel par_ws2, otherwise T chunks of W nonzeros per tile (4
+      // or 8: the two compiled shapes of the tile kernel)
       const bool ws2 = W == 32 && N <= 2 && h->tune.parws_impl == 2;
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
       const long long chunks = (h->nnz + 31) / 32;
-      // N = 1 / 2 / 4: par_ws3 (plans without long rows) on tiles of ~chunks /
+      // N = 1 … 4: par_ws3 (long rows too unless parws3 = 1) on tiles of ~chunks /
       // 16K chunks (measured best on R-MAT uniform s16..s22: 4 .. 64); with long
       // rows, par_ws2 (N <= 2) on its own tiles (the largest power of two <= 64
       // that still gives >= 8 waves of 32 resident warps per SM) or the tile kernel
-      bool ws3 = W == 32 && (N <= 2 || N == 4) && h->tune.parws_impl == 2 && h->tune.parws3 != 0;
+      bool ws3 = W == 32 && N <= 4 && h->tune.parws_impl == 2 && h->tune.parws3 != 0;
       auto ws_cpt = [&](bool three) {
         long long c = h->tune.parws_cpt;
         if (c > 0) return c;

@@ -139,7 +139,7 @@ struct Tuning {
   long long l2_persist = 0;      // 1 = access-policy window over X on every spmm
   long long parws_impl = 2;      // par-ws at lane_width 32, N <= 2: 2 = streaming head-flag kernel (par_ws2.cuh), 1 = tile kernel
   long long parws_cpt = 0;       // par_ws2 chunks per tile (0 = automatic)
-  long long parws3 = 2;          // par-ws at W 32, N = 1 / 2 / 4: par_ws3.cuh (2 = every plan, 1 = plans without long rows), 0 = par_ws2 / tile kernel
+  long long parws3 = 2;          // par-ws at W 32, N = 1 … 4: par_ws3.cuh (2 = every plan, 1 = plans without long rows), 0 = par_ws2 / tile kernel
   long long sell_cfg = 0;        // lane-per-job sweep shape (launch_sell.cu)
   long long seq_impl = 2;        // seq-ws, seq_chunk <= kSellMaxChunk: 2 = lane-per-job sweep (sell_kernels.cuh) at N = 32, 3 = also at N % 32 == 0, 1 = tile sweep only
   void from_env();
@@ -264,7 +264,7 @@ void launch_par_rs(const ParLaunch& a, int W, int vl, bool aligned, cudaStream_t
 void launch_par_ws(const ParLaunch& a, int W, int T, bool aligned, cudaStream_t s);
 void launch_par_ws64(const ParLaunch& a, float* slots, cudaStream_t s);  // lane_width 64
 void launch_par_ws2(const ParLaunch& a, const unsigned* hflag, bool aligned, cudaStream_t s);
-// W 32, N = 1 / 2 / 4; rid_ident: no empty rows; long_rows: the plan has long rows (H / T partials)
+// W 32, N = 1 … 4; rid_ident: no empty rows; long_rows: the plan has long rows (H / T partials)
 void launch_par_ws3(const ParLaunch& a, const unsigned* hflag, bool rid_ident, bool aligned, bool long_rows,
                     cudaStream_t s);  // W 32, N <= 2
 void launch_hubs(spmk_csr_s* h, const Plan& hub, spmk_kernel_id id, int W, int L, const float* d_x, int N,

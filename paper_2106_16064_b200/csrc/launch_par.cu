@@ -210,6 +210,7 @@ void launch_par_ws3_t(const ParWs2Args& A, cudaStream_t s) {
   const unsigned grid = (unsigned)((A.p.nunits + 7) / 8);
   if (A.p.N == 1) par_ws3_kernel<1, LONG><<<grid, 256, 0, s>>>(A);
   else if (A.p.N == 2) par_ws3_kernel<2, LONG><<<grid, 256, 0, s>>>(A);
+  else if (A.p.N == 3) par_ws3_kernel<3, LONG><<<grid, 256, 0, s>>>(A);
   else par_ws3_kernel<4, LONG><<<grid, 256, 0, s>>>(A);
   LAUNCHED(1);
 }

@@ -1,5 +1,4 @@
-// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for N = 1 / 2 / 4 on
-// matrices without long rows: the par_ws2 sweep with one chunk per
+// par_ws3.cuh — par-ws (north_star d) at lane_width 32 for N = 1 … 4: the par_ws2 sweep with one chunk per
 // iteration and only the arithmetic that case needs.
 //
 // Same arithmetic as spmm_par_balanced (kernels.hpp:232-330) for W = 32 and
@@ -41,6 +40,9 @@ __device__ __forceinline__ void ws3_gather(const float* X, int c, bool vec, floa
       x[0] = ld_x(r);
       x[1] = ld_x(r + 1);
     }
+  } else if constexpr (CT == 3) {
+#pragma unroll
+    for (int j = 0; j < CT; ++j) x[j] = ld_x(r + j);
   } else {
     if (vec) {
       const float4 t = ld_x4(r);
@@ -158,9 +160,9 @@ par_ws3_kernel(const ParWs2Args A) {
       float* y = a.Y + (size_t)(unsigned)row * CT;
       if constexpr (CT == 1) {
         st_y(y, t[0]);
-      } else if (vec) {  // X and Y 16-byte aligned: rows of CT floats are 4 CT-byte aligned
+      } else if (CT != 3 && vec) {  // X and Y 16-byte aligned: rows of CT floats are 4 CT-byte aligned
         if constexpr (CT == 2) st_y2(y, t[0], t[1]);
-        else st_y4(y, t[0], t[1], t[2], t[3]);
+        else if constexpr (CT == 4) st_y4(y, t[0], t[1], t[2], t[3]);
       } else {
 #pragma unroll
         for (int j = 0; j < CT; ++j) st_y(y + j, t[j]);

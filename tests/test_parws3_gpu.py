@@ -46,7 +46,7 @@ def same_bits(y, want):
     assert np.array_equal(y[~yn].view(np.uint32), want[~wn].view(np.uint32))
 
 
-@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
 @pytest.mark.parametrize("empty_rows", [False, True])
 @pytest.mark.parametrize("cpt", [0, 4, 8, 64])
 def test_bit_exact(orc, empty_rows, cpt, n):
@@ -68,7 +68,7 @@ def test_bit_exact(orc, empty_rows, cpt, n):
         assert np.all(y[e] == 0) and not np.any(np.signbit(y[e]))
 
 
-@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
 def test_long_rows(orc, n):
     """Rows longer than a tile make the plan carry long rows (per-chunk H
     partials, owner prefixes in T, fix-up): bit-exact through par_ws3's long
@@ -88,7 +88,7 @@ def test_long_rows(orc, n):
         same_bits(run(d, x, parws3=2, parws_cpt=cpt), want)  # par_ws3 with H / T partials
 
 
-@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 3, 4])
 def test_inf_nan_in_x(orc, n):
     """Dead lanes gather X row 0 and live runs never read them: inf / NaN in
     X (row 0 too) give the reference's bits."""
@@ -103,7 +103,7 @@ def test_inf_nan_in_x(orc, n):
     same_bits(run(d, x, parws3=1, parws_cpt=0), orc.spmm(csr_of(a), 1, x))
 
 
-@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("n", [2, 3, 4])
 def test_unaligned_operands(orc, n):
     """X / Y views 4 bytes off a 16-byte boundary: scalar loads and stores,
     same bits."""
