@@ -97,13 +97,16 @@ def test_tuning_knobs_keep_bits(mat):
     """Every performance knob picks tile shapes / kernel paths, never a
     summation order: par-ws through the tile kernel (parws_impl=1) and the
     streaming kernel (2) at several tile sizes give identical bits."""
-    x = torch.randn(mat.num_cols, 2, device="cuda")
-    ref = mat.spmm(spmk.kParBalanced, x).clone()
-    try:
-        for impl, cpt in ((1, 0), (2, 4), (2, 16), (2, 64)):
-            mat.set_tuning("parws_impl", impl)
-            mat.set_tuning("parws_cpt", cpt)
-            assert torch.equal(mat.spmm(spmk.kParBalanced, x), ref), (impl, cpt)
-    finally:
-        mat.set_tuning("parws_impl", 2)
-        mat.set_tuning("parws_cpt", 0)
+    for n in (1, 2, 3, 4):
+        x = torch.randn(mat.num_cols, n, device="cuda")
+        ref = mat.spmm(spmk.kParBalanced, x).clone()
+        try:
+            for impl, ws3, cpt in ((1, 0, 0), (2, 0, 4), (2, 0, 16), (2, 0, 64), (2, 1, 8), (2, 2, 4), (2, 2, 64)):
+                mat.set_tuning("parws_impl", impl)
+                mat.set_tuning("parws3", ws3)
+                mat.set_tuning("parws_cpt", cpt)
+                assert torch.equal(mat.spmm(spmk.kParBalanced, x), ref), (n, impl, ws3, cpt)
+        finally:
+            mat.set_tuning("parws_impl", 2)
+            mat.set_tuning("parws3", 2)
+            mat.set_tuning("parws_cpt", 0)
