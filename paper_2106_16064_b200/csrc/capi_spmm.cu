@@ -266,8 +266,9 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
       const int T = h->tune.parws_t == 8 ? 8 : 4;
       const long long CH = W;
       const long long chunks = (h->nnz + 31) / 32;
-      // N = 1 … 4: par_ws3 (long rows too unless parws3 = 1) on tiles of ~chunks /
-      // 16K chunks (measured best on R-MAT uniform s16..s22: 4 .. 64); with long
+      // N = 1 … 4: par_ws3 (long rows too unless parws3 = 1) on ~16K tiles
+      // (measured best on R-MAT uniform s16..s22 and banded s20: 4 .. 64; 8K or
+      // 32K tiles up to 1.3x slower); with long
       // rows, par_ws2 (N <= 2) on its own tiles (the largest power of two <= 64
       // that still gives >= 8 waves of 32 resident warps per SM) or the tile kernel
       bool ws3 = W == 32 && N <= 4 && h->tune.parws_impl == 2 && h->tune.parws3 != 0;
@@ -275,8 +276,8 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         long long c = h->tune.parws_cpt;
         if (c > 0) return c;
         c = 4;
-        if (three)
-          while (c < 64 && chunks > 16384LL * c) c *= 2;
+        if (three)  // tiles closest to 16K (log scale): double while > 16K * sqrt(2)
+          while (c < 64 && chunks > 23170LL * c) c *= 2;
         else
           while (c < 64 && chunks / (c * 2) >= 8LL * 148 * 32) c *= 2;
         return c;
