@@ -276,10 +276,12 @@ spmk_status run_spmm(spmk_csr_s* h, spmk_kernel_id id, const spmk_kernel_config&
         long long c = h->tune.parws_cpt;
         if (c > 0) return c;
         c = 4;
-        if (three)  // tiles closest to 16K (log scale): double while > 16K * sqrt(2)
+        if (three) {  // tiles closest to 16K (log scale): double while > 16K * sqrt(2)
+          if (chunks < 65536) c = 8;  // small (cfg1): 8.5 -> 7.9 us per call from a graph, 15.2 -> 15.1 flushed
           while (c < 64 && chunks > 23170LL * c) c *= 2;
-        else
+        } else {
           while (c < 64 && chunks / (c * 2) >= 8LL * 148 * 32) c *= 2;
+        }
         return c;
       };
       long long TS = ws3 ? CH * ws_cpt(true) : (ws2 ? CH * ws_cpt(false) : CH * T);
