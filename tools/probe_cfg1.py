@@ -23,7 +23,11 @@ def graph_us(**tune):
         best = min(best, e0.elapsed_time(e1) * 1e3 / 100)
     return best
 if QUICK:
-    print(sys.argv[1], "par-ws", round(graph_us(), 2), "par-rs", end=" ")
+    if len(sys.argv) > 3:  # extra knob=value pairs for the par-ws line
+        for kv in sys.argv[3:]:
+            k_, v_ = kv.split("=")
+            a.set_tuning(k_, int(v_))
+    print(sys.argv[1], sys.argv[3:], "par-ws", round(graph_us(), 2), "par-rs", end=" ")
     kid = spmk.kParRowSplit
     print(round(graph_us(), 2))
     sys.exit(0)
