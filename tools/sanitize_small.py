@@ -11,7 +11,7 @@ import paper_2106_16064_b200 as spmk  # noqa: E402
 
 for skew in ((0.57, 0.19, 0.19, 0.05), (0.25, 0.25, 0.25, 0.25)):
     d = spmk.DeviceCsr.generate_rmat(10, 8, skew, 3)
-    for n in (1, 3, 4, 8, 16, 32, 64):
+    for n in (1, 2, 3, 4, 8, 16, 32, 64):
         x = spmk.make_dense_device(d.num_cols, n, 5 + n)
         for kid in spmk.kAllKernels:
             for cfg in (None, spmk.KernelConfig(lane_width=8, seq_chunk=16)):
